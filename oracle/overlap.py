@@ -1,0 +1,104 @@
+"""O5/O6 — overlap resolution and hat weights (Table 1 :389-418,
+Table 2 :524-547).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Readings (R5-R7):
+* Overlap layers per level/direction (identical on both sides on a uniform
+  grid): count the neighbour-element nodes whose face distance d (reference
+  units, element width 2) satisfies d <= delta_ref (GLL) or d < delta_ref (GL),
+  tolerance 1e-12, delta_ref = 2 delta_O / Delta_d; then max with the floor and
+  cap at n = P+1.  FixedNodes(n_o) -> min(n_o, n).
+* delta_ref used by the weight: Relative/MaxRelative -> the geometric 2 delta_O/Delta;
+  FixedNodes(n_o), or a count raised by the floor -> midpoint between the n_o-th
+  and (n_o+1)-th neighbour node distance (2 if n_o = n).
+* Hat weight (Fig. 2 caption): xi_H = xi in the own element,
+  xi -/+ 2 in the left/right neighbour; h = min(delta_ref, 1) (0 if the side has
+  no overlap layer); t = (1 + h - |xi_H|) / (2 h) clipped to [0, 1];
+  w = q(t) = 10 t^3 - 15 t^4 + 6 t^5.  The quintic itself is the documented
+  choice (the exact one is in the absent [Stiller2016]): PARITY UNPINNED beyond
+  its stated shape (0 at the subdomain boundary, 1 on the non-overlapped core,
+  piecewise quintic) and partition of unity, which tests/ check.
+"""
+import numpy as np
+from .basis import GLL, GL, face_distances
+
+OVL_NODES, OVL_REL, OVL_MAXREL = 0, 1, 2
+TOL = 1e-12
+
+
+def _count(basis, P, delta_ref):
+    d = face_distances(basis, P)
+    if basis == GLL:
+        return int(np.sum(d <= delta_ref + TOL))
+    return int(np.sum(d < delta_ref - TOL))
+
+
+def _midpoint(basis, P, n_o):
+    d = face_distances(basis, P)
+    n = P + 1
+    if n_o >= n:
+        return 2.0
+    if n_o == 0:
+        return 0.0
+    return 0.5 * (d[n_o - 1] + d[n_o])
+
+
+def resolve_overlap(mode, value, floor, basis, P, deltas):
+    """Return [(n_o, delta_ref)] for the three directions at degree P."""
+    n = P + 1
+    out = []
+    dmax = max(deltas)
+    for dd in deltas:
+        if mode == OVL_NODES:
+            n_o = min(int(value), n)
+            n_o2 = min(max(n_o, floor), n)
+            out.append((n_o2, _midpoint(basis, P, n_o2)))
+            continue
+        if mode == OVL_REL:
+            delta_O = value * dd
+        elif mode == OVL_MAXREL:
+            delta_O = min(value * dmax, dd)
+        else:
+            raise ValueError("unknown overlap mode")
+        dref = 2.0 * delta_O / dd
+        c = min(_count(basis, P, dref), n)
+        if floor > c:
+            c = min(floor, n)
+            dref = _midpoint(basis, P, c)
+        out.append((c, dref))
+    return out
+
+
+def quintic(t):
+    t = np.clip(t, 0.0, 1.0)
+    return t * t * t * (10.0 - 15.0 * t + 6.0 * t * t)
+
+
+def hat_weight(xi_h, h):
+    """w_H(xi_H) for a symmetric subdomain with transition half-width h on both sides."""
+    xi_h = np.asarray(xi_h, dtype=float)
+    if h <= 0.0:
+        return np.where(np.abs(xi_h) <= 1.0 + TOL, 1.0, 0.0)
+    return quintic((1.0 + h - np.abs(xi_h)) / (2.0 * h))
+
+
+def window_1d(basis, P, n_o):
+    """Window of one direction: list of (element offset, local node) and the xi_H of each node."""
+    from .basis import nodes_weights
+    x, _ = nodes_weights(basis, P)
+    n = P + 1
+    pos, xih = [], []
+    for t in range(n - n_o, n):
+        pos.append((-1, t)); xih.append(x[t] - 2.0)
+    for i in range(n):
+        pos.append((0, i)); xih.append(x[i])
+    for t in range(n_o):
+        pos.append((1, t)); xih.append(x[t] + 2.0)
+    return pos, np.array(xih)
+
+
+def weights_1d(basis, P, n_o, delta_ref):
+    _, xih = window_1d(basis, P, n_o)
+    h = min(delta_ref, 1.0) if n_o > 0 else 0.0
+    return hat_weight(xih, h)

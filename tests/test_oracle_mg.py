@@ -1,0 +1,132 @@
+"""Pins for oracle O4 (transfers), O9 (coarse A_0^+), O10 (V-cycle), O11 (PCG), and O-mf vs O-dense.
+
+* transfers reproduce degree-P_{l-1} polynomials; <I c, f> = <c, I^T f>
+* coarse: A_0 x = f_0 for consistent f_0, 1^T x = 0, equals numpy.linalg.pinv  (Alg. 1 l.295)
+* V-cycle: fixed point; error-propagation spectral radius < 1;
+  translation invariance; "about two orders of magnitude" per V(1,1) at high P
+  with delta_O = 0.08 Delta x
+* PCG: exact preconditioner -> 1 iteration; MG-CG beats MG at n_o = 1 (Table 1 rows 1/2)
+"""
+import numpy as np
+import pytest
+
+from oracle.basis import GLL, GL
+from oracle.dense import DenseHierarchy, assemble_A, node_coords
+from oracle.mf import MFHierarchy
+from oracle import mg
+from workloads import get_config, uniform_zero_mean
+from workloads.configs import OverlapSpec
+
+
+def _H(cfg, ne, cls=DenseHierarchy):
+    c = get_config(cfg, ne)
+    return c, cls(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+
+
+@pytest.mark.parametrize("basis", [GLL, GL])
+def test_transfers(basis):
+    H = MFHierarchy((3, 3, 3), (1.0, 1.0, 1.0), 8, basis, 2.0, None)
+    rng = np.random.default_rng(0)
+    for l in range(1, H.L + 1):
+        Pc = H.Pl[l - 1]
+        Xc, Yc, Zc = node_coords(H.ne, H.length, Pc, basis)
+        Xf, Yf, Zf = node_coords(H.ne, H.length, H.Pl[l], basis)
+        # element-local polynomial of degree Pc (per-element coordinates are enough: the
+        # interpolation is element-wise, so use a global polynomial which is one per element)
+        poly = lambda X, Y, Z: X ** Pc - 2 * Y * Z ** (Pc - 1) + 0.5 * X * Y
+        up = H.prolong(l, poly(Xc, Yc, Zc))
+        assert np.max(np.abs(up - poly(Xf, Yf, Zf))) < 1e-12
+        c = rng.standard_normal(H.ndofs(l - 1))
+        f = rng.standard_normal(H.ndofs(l))
+        assert abs(H.prolong(l, c) @ f - c @ H.restrict(l, f)) < 1e-11 * np.linalg.norm(f) * np.linalg.norm(c)
+
+
+@pytest.mark.parametrize("basis", [GLL, GL])
+def test_coarse_pseudoinverse(basis):
+    H = DenseHierarchy((3, 3, 3), (1.0, 1.0, 1.0), 2, basis, 2.0, OverlapSpec(1, 0.08, 1))
+    A0 = H.levels[0].A.toarray()
+    f = np.random.default_rng(1).standard_normal(len(A0))
+    x = H.coarse(f)
+    assert np.allclose(x, np.linalg.pinv(A0) @ f, atol=1e-11 * np.abs(x).max())
+    fp = f - f.mean()
+    assert np.linalg.norm(A0 @ x - fp) < 1e-12 * np.linalg.norm(fp)
+    assert abs(x.sum()) < 1e-12 * np.abs(x).max() * len(x)
+
+
+def test_vcycle_fixed_point():
+    c, H = _H("c1", 4)
+    u = np.random.default_rng(5).uniform(-1, 1, c.ndofs)
+    u -= u.mean()
+    f = H.apply(H.L, u)
+    assert np.max(np.abs(mg.vcycle(H, u, f) - u)) < 1e-11
+
+
+def test_error_propagation_spectral_radius():
+    H = DenseHierarchy((3, 3, 3), (1.0, 1.0, 1.0), 2, GLL, 2.0, OverlapSpec(0, 1, 0))
+    N = H.ndofs(H.L)
+    A = H.levels[H.L].A
+    T = np.empty((N, N))
+    I = np.eye(N)
+    for j in range(N):
+        T[:, j] = I[:, j] - mg.vcycle(H, np.zeros(N), A @ I[:, j])
+    ev = np.sort(np.abs(np.linalg.eigvals(T)))[::-1]
+    # one eigenvalue 1 (the constant null vector is invisible to the residual) ...
+    assert abs(ev[0] - 1.0) < 1e-8
+    # ... and the cycle contracts everything else
+    assert ev[1] < 0.5, ev[:4]
+
+
+def test_translation_invariance():
+    c, H = _H("c1", 4, MFHierarchy)
+    n = c.P + 1
+    f = uniform_zero_mean(c.ndofs, 0)
+    F = f.reshape(4, 4, 4, n ** 3)                        # [ez, ey, ex, node]
+    fs = np.roll(F, 1, axis=2).ravel()                    # shift by one element in x
+    a = mg.vcycle(H, np.zeros_like(f), f).reshape(4, 4, 4, n ** 3)
+    b = mg.vcycle(H, np.zeros_like(f), fs).reshape(4, 4, 4, n ** 3)
+    assert np.max(np.abs(np.roll(a, 1, axis=2) - b)) < 1e-12 * np.max(np.abs(a))
+
+
+@pytest.mark.parametrize("P", [8, 16])
+def test_two_orders_per_cycle(P):
+    # recommended method GLL, delta_O = 0.08 Delta x: "about two orders of magnitude within a
+    # single V(1,1) cycle"; the first cycle from u=0 must reduce >= 10^1.5
+    H = MFHierarchy((4, 4, 4), (1.0, 1.0, 1.0), P, GLL, 2.0, OverlapSpec(1, 0.08, 0))
+    f = uniform_zero_mean(H.ndofs(H.L), 0)
+    u, hist = mg.mg_solve(H, f, maxcycles=3)
+    assert hist[1] / hist[0] < 10 ** -1.5, hist
+    assert mg.rho(hist) < 0.2
+
+
+def test_pcg_exact_preconditioner_one_iteration():
+    H = DenseHierarchy((3, 3, 3), (1.0, 1.0, 1.0), 2, GLL, 2.0, OverlapSpec(0, 1, 0))
+    A = H.levels[H.L].A.toarray()
+    Ap = np.linalg.pinv(A)
+    f = uniform_zero_mean(len(A), 0)
+    u, hist = mg.pcg(H, f, precond=lambda r: Ap @ r, rtol=1e-10)
+    assert len(hist) == 2 and hist[-1] < 1e-10 * hist[0]
+
+
+def test_mgcg_beats_mg_with_one_node_overlap():
+    # Table 1 rows 1 vs 2: MG-CG converges faster than MG at n_o = 1
+    H = MFHierarchy((4, 4, 4), (1.0, 1.0, 1.0), 8, GLL, 2.0, OverlapSpec(0, 1, 0))
+    f = uniform_zero_mean(H.ndofs(H.L), 0)
+    _, h_mg = mg.mg_solve(H, f, rtol=1e-8, maxcycles=60)
+    _, h_cg = mg.pcg(H, f, rtol=1e-8, maxit=60)
+    assert h_cg[-1] <= 1e-8 * h_cg[0] and len(h_cg) < len(h_mg)
+
+
+@pytest.mark.parametrize("cfg,ne", [("c1", 4), ("c2", 3), ("c5", 3)])
+def test_mf_matches_dense_vcycle(cfg, ne):
+    c = get_config(cfg, ne)
+    if cfg == "c5":
+        c = get_config("c5", 3)
+        c = type(c)(c.name, c.ne, c.length, 4, c.basis, c.overlap)     # P=4 keeps dense LU small
+    Hd = DenseHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    Hm = MFHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    f = uniform_zero_mean(Hd.ndofs(Hd.L), 0)
+    a = mg.vcycle(Hd, np.zeros_like(f), f)
+    b = mg.vcycle(Hm, np.zeros_like(f), f)
+    tol = 1e-12 if cfg != "c5" else 1e-8            # c5: cond(A_ss) ~ 1e6 (see test_oracle_schwarz)
+    assert np.max(np.abs(a - b)) < tol * np.max(np.abs(a))
+    assert np.max(np.abs(Hd.apply(Hd.L, a) - Hm.apply(Hm.L, a))) < 1e-11 * np.max(np.abs(Hd.apply(Hd.L, a)))
