@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 V(1,1) p-multigrid cycles (arXiv:1612.04796, Algorithm 1) on B200.
+
+Contract (one JSON line on rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+A step = one V(1,1) cycle (all hot-path rows: residual/apply, Schwarz FDM solves + weighted
+scatter on every level, transfers, coarse solve) over the config's synthetic input.
+Default workload: BASELINE.json configs[2] ("c3": 16^3 elements, P=16 GLL, 20.1M DOF, the
+config BASELINE.json marks "for throughput and roofline"); every other config can be benched
+with --config.  N>1: independent replicas, one per GPU ("replicas only").
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 V(1,1) DOF/s at 1 B200; residual reduction/cycle; % of FP64/HBM roofline"
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 TF: 64 DFMA/clk/SM at 1965 MHz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-kernels", action="store_true", default=True)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------------
+def cycle_model(g, c):
+    """Algorithmic flop / byte counts of one V(1,1) cycle."""
+    L = g.L
+    NL = g.ndofs(L)
+    flops = 0.0
+    fdm_flops_top = 0.0
+    for l in range(1, L + 1):
+        n = 2 ** l + 1
+        Nl = g.ndofs(l)
+        Ne = Nl // n ** 3
+        _, m = g.level_overlap(l)
+        Mw = m[0] * m[1] * m[2]
+        FA = (6 * n + (24 if c.basis == 0 else 48)) * Nl
+        FS = (4 * (m[0] + m[1] + m[2]) + 4) * Mw * Ne
+        FT = 7 * (2 ** (l - 1) + 1) * Nl
+        flops += 3 * FA + 2 * FS + FT
+        if l == L:
+            fdm_flops_top = FS
+    bytes_ = 120.0 * NL * 8.0 / 7.0
+    return flops, bytes_, fdm_flops_top
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    from paper_1612_04796_b200 import DG
+    from workloads import get_config, uniform_zero_mean
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    c = get_config(args.config)
+    g = DG(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    N = g.ndofs()
+    f_host = torch.from_numpy(uniform_zero_mean(N, 0)).pin_memory()
+    f = f_host.to(dev)
+    u = torch.zeros(N, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # residual history (reduction per cycle) from the warm-up cycles
+    r0 = float(np.sqrt(g.dot(f, f)))
+    hist = [r0]
+    for _ in range(args.warmup):
+        g.pmg_vcycle(u, f)
+        res = g.residual(u, f)
+        hist.append(float(np.sqrt(g.dot(res, res))))
+    rho = [hist[i + 1] / hist[i] for i in range(len(hist) - 1)]
+    u.zero_()
+
+    # ---- timed region: K cycles, device-timed with CUDA events, inputs > L2 (no flush)
+    clocks = ClockSampler(local_rank)
+    g.profile(True)
+    g.profile_read(reset=True)
+    launches0 = g.launch_count()
+    barrier()
+    clocks.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        g.pmg_vcycle(u, f)
+    ev1.record(stream)
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = g.launch_count() - launches0
+    prof = g.profile_read(reset=True)
+    g.profile(False)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = N * world * args.steps / (ms_total / 1e3)
+
+    # ---- e2e: host buffers through the public API (H2D of u and f, cycle, D2H of u)
+    u_host = torch.zeros(N, dtype=torch.float64).pin_memory()
+    out_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        ud = u_host.to(dev, non_blocking=True)
+        fd = f_host.to(dev, non_blocking=True)
+        g.pmg_vcycle(ud, fd)
+        out_host.copy_(ud, non_blocking=True)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ud = u_host.to(dev, non_blocking=True)
+        fd = f_host.to(dev, non_blocking=True)
+        g.pmg_vcycle(ud, fd)
+        out_host.copy_(ud, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- roofline of the dominant kernel (Schwarz FDM solve on the top level)
+    flops, bytes_, fdm_flops = cycle_model(g, c)
+    top = g.L
+    fdm_ms, fdm_cnt = prof.get(("fdm", top), (0.0, 0))
+    fdm_avg_ms = fdm_ms / max(fdm_cnt, 1)
+    total_prof = sum(v[0] for v in prof.values())
+    peak_tf = FP64_NOMINAL_TFLOPS
+    achieved_tf = fdm_flops / (fdm_avg_ms / 1e3) / 1e12 if fdm_avg_ms > 0 else None
+    kernels = {"%s@l%d" % k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    cyc_t_roof = max(flops / (peak_tf * 1e12), bytes_ / 6554.6e9)
+    out = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "%s: %s, %dx%dx%d elements, P=%d %s, %d DOF, V(1,1) cycle"
+                   % (c.name, "periodic box %s" % (c.length,), c.ne[0], c.ne[1], c.ne[2], c.P,
+                      "GLL" if c.basis == 0 else "GL", N),
+                   "overlap": {"mode": c.overlap.mode, "value": c.overlap.value, "floor": c.overlap.floor},
+                   "l2": "inputs larger than L2 (u, f, r: %.0f MB each); no flush" % (N * 8 / 1e6),
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "e2e": {"value": N * world / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 16 * N,
+                "d2h_bytes_per_step": 8 * N},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": None,
+                     "kernel": "k_fdm (Schwarz fast-diagonalisation solve, top level)",
+                     "share_of_step": (fdm_ms / total_prof) if total_prof else None,
+                     "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (guide unit counts)"},
+        "cycle_roofline": {"flop_per_cycle": flops, "bytes_per_cycle": bytes_,
+                           "t_roof_ms": cyc_t_roof * 1e3, "frac": cyc_t_roof * 1e3 / ms_step},
+        "residual_reduction_per_cycle": rho,
+        "kernels": kernels,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.config)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return out
+
+
+def cpu_baseline(name, steps=3):
+    """The oracle's matrix-free V(1,1) (oracle.mf, untuned) on a bounded sample of the workload."""
+    import numpy as np
+    from workloads import get_config, uniform_zero_mean
+    from oracle.mf import MFHierarchy
+    from oracle import mg
+    c = get_config(name)
+    ne = tuple(min(x, 8) for x in c.ne)
+    s = get_config(name, ne)
+    H = MFHierarchy(s.ne, s.length, s.P, s.basis, s.penalty, s.overlap)
+    f = uniform_zero_mean(s.ndofs, 0)
+    u = mg.vcycle(H, np.zeros_like(f), f)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        u = mg.vcycle(H, u, f)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": s.ndofs / t, "unit": "DOF/s", "cores": cores, "kind": "oracle",
+            "sample": "oracle.mf V(1,1) on %s's P/basis/overlap with %dx%dx%d elements (%d DOF), median of %d"
+                      % (name, ne[0], ne[1], ne[2], s.ndofs, steps),
+            "s_per_cycle": t}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cb = None
+    import numpy as np
+    from workloads import get_config, uniform_zero_mean
+    from oracle.mf import MFHierarchy
+    from oracle import mg
+    c = get_config(args.config)
+    ne = tuple(min(x, 8) for x in c.ne)
+    s = get_config(args.config, ne)
+    H = MFHierarchy(s.ne, s.length, s.P, s.basis, s.penalty, s.overlap)
+    f = uniform_zero_mean(s.ndofs, 0)
+    u = np.zeros_like(f)
+    for _ in range(args.warmup):
+        u = mg.vcycle(H, u, f)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        u = mg.vcycle(H, u, f)
+    t = (time.perf_counter() - t0) / args.steps
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count()
+    v = s.ndofs / t
+    sample = "oracle.mf V(1,1) on %s's P/basis/overlap with %dx%dx%d elements (%d DOF)" % (
+        args.config, ne[0], ne[1], ne[2], s.ndofs)
+    return {"metric": METRIC, "value": v, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "%s (CPU oracle sample)" % args.config},
+            "cpu_baseline": {"value": v, "unit": "DOF/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,559 @@
+// FP64 kernels of the p-multigrid V(1,1) hot path on B200 (sm_100a).
+// arXiv:1612.04796; PAPER.md line numbers cited per kernel.
+//
+// Layout: element-major vectors, element e = ex + nx*(ey + ny*ez), node i + n*(j + n*k).
+// Face-trace buffer T (per level): T[((e*3 + d)*4 + q)*n^2 + p], q = 0 left value,
+// 1 left (2/D)-derivative, 2 right value, 3 right derivative; p = in-face node index
+// (x-faces: j + n k, y-faces: i + n k, z-faces: i + n j).
+#include "kernels.cuh"
+
+namespace pmg {
+
+namespace {
+
+__device__ __forceinline__ int wrap(int a, int n) { return a < 0 ? a + n : (a >= n ? a - n : a); }
+
+// ---------------------------------------------------------------------------------------------
+// Face traces (value and normal derivative on both faces of every direction) — the data the
+// rank-2 neighbour couplings of Eq. 7's block-tridiagonal L_* need.
+__global__ void k_traces(LevelDev L, const double *__restrict__ u, double *__restrict__ T) {
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int e = blockIdx.x;
+  const double *ue = u + (long long)e * n3;
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = L.tr[d];
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = __ldg(ue + base + i * stride);
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
+// Operator apply v = A u (Eq. 7) or residual r = f - A u (Eq. 8), sum-factorised per element.
+__global__ void k_apply(LevelDev L, const double *__restrict__ u, const double *__restrict__ T,
+                        const double *__restrict__ f, double *__restrict__ out) {
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int e = blockIdx.x;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  const int ecoord[3] = {ex, ey, ez};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  int nbL[3], nbR[3];
+  for (int d = 0; d < 3; ++d) {
+    int c[3] = {ex, ey, ez};
+    c[d] = wrap(ecoord[d] - 1, edim[d]);
+    nbL[d] = c[0] + L.nx * (c[1] + L.ny * c[2]);
+    c[d] = wrap(ecoord[d] + 1, edim[d]);
+    nbR[d] = c[0] + L.nx * (c[1] + L.ny * c[2]);
+  }
+  const double *ue = u + (long long)e * n3;
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int i = t % n, j = (t / n) % n, k = t / n2;
+    const int idx[3] = {i, j, k};
+    const int pface[3] = {j + n * k, i + n * k, i + n * j};
+    const int stride[3] = {1, n, n2};
+    double s[3];
+    for (int d = 0; d < 3; ++d) {
+      const int id = idx[d];
+      const double *Dr = L.D[d] + id * n;
+      const double *line = ue + (t - id * stride[d]);
+      double acc = 0;
+      for (int q = 0; q < n; ++q) acc += Dr[q] * __ldg(line + q * stride[d]);
+      const double *TR = T + ((long long)nbR[d] * 3 + d) * 4 * n2;
+      const double *TL = T + ((long long)nbL[d] * 3 + d) * 4 * n2;
+      const double tvR = TR[pface[d]], tdR = TR[n2 + pface[d]];
+      const double tvL = TL[2 * n2 + pface[d]], tdL = TL[3 * n2 + pface[d]];
+      const double *tr = L.tr[d];
+      const double mu = L.mu[d];
+      acc += tr[id] * (-0.5 * tdR - mu * tvR) + tr[n + id] * (0.5 * tvR)
+           + tr[2 * n + id] * (0.5 * tdL - mu * tvL) + tr[3 * n + id] * (-0.5 * tvL);
+      s[d] = acc;
+    }
+    const double mx = L.mass[0][i], my = L.mass[1][j], mz = L.mass[2][k];
+    const double v = mz * my * s[0] + mz * mx * s[1] + my * mx * s[2];
+    const long long g = (long long)e * n3 + t;
+    out[g] = f ? f[g] - v : v;
+  }
+}
+
+// Generic 1D contraction along one axis of a (d0,d1,d2) block (d0 fastest):
+// out[.., o, ..] = sum_k A[o*so + k*sk] * in[.., k, ..]; generic pointers (smem or global).
+__device__ void contract_axis(const double *in, double *out, int d0, int d1, int d2, int ax,
+                              const double *A, int so, int sk, int nout) {
+  int od[3] = {d0, d1, d2};
+  const int K = od[ax];
+  od[ax] = nout;
+  const int total = od[0] * od[1] * od[2];
+  const int istr[3] = {1, d0, d0 * d1};
+  const int st = istr[ax];
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    int p[3];
+    p[0] = t % od[0];
+    const int r = t / od[0];
+    p[1] = r % od[1];
+    p[2] = r / od[1];
+    const int o = p[ax];
+    p[ax] = 0;
+    const double *src = in + p[0] + p[1] * d0 + p[2] * d0 * d1;
+    const double *a = A + o * so;
+    double acc = 0;
+    for (int k = 0; k < K; ++k) acc += a[k * sk] * src[k * st];
+    out[t] = acc;
+  }
+}
+
+// Weighted-Schwarz subdomain solve by fast diagonalisation (Eqs. 9-10):
+// gather the element-centred window of r, apply S_x^T, S_y^T, S_z^T, divide by
+// lam_x + lam_y + lam_z, apply S_z, S_y, S_x, multiply by W = W_z (x) W_y (x) W_x.
+// One CTA per subdomain; result window stored in Z[s*Mw + ...].
+__global__ void k_fdm(LevelDev L, const double *__restrict__ r, double *__restrict__ Z,
+                      double *__restrict__ scr, int use_smem) {
+  extern __shared__ double sm[];
+  const int n = L.n, n3 = n * n * n;
+  const int mx = L.m[0], my = L.m[1], mz = L.m[2], Mw = L.Mw;
+  const int e = blockIdx.x;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  double *X, *Y;
+  if (use_smem) { X = sm; Y = sm + Mw; }
+  else { X = scr + (long long)e * Mw; Y = Z + (long long)e * Mw; }
+  // gather
+  for (int w = threadIdx.x; w < Mw; w += blockDim.x) {
+    const int a = w % mx, b = (w / mx) % my, c = w / (mx * my);
+    const int win[3] = {a, b, c};
+    const int ec[3] = {ex, ey, ez};
+    const int edim[3] = {L.nx, L.ny, L.nz};
+    int el[3], loc[3];
+    for (int d = 0; d < 3; ++d) {
+      const int no = L.no[d];
+      int o, li;
+      if (win[d] < no) { o = -1; li = n - no + win[d]; }
+      else if (win[d] < no + n) { o = 0; li = win[d] - no; }
+      else { o = 1; li = win[d] - no - n; }
+      el[d] = wrap(ec[d] + o, edim[d]);
+      loc[d] = li;
+    }
+    const long long g = (long long)(el[0] + L.nx * (el[1] + L.ny * el[2])) * n3 + loc[0]
+                      + n * (loc[1] + n * loc[2]);
+    X[w] = __ldg(r + g);
+  }
+  __syncthreads();
+  contract_axis(X, Y, mx, my, mz, 0, L.S[0], 1, mx, mx); __syncthreads();
+  contract_axis(Y, X, mx, my, mz, 1, L.S[1], 1, my, my); __syncthreads();
+  contract_axis(X, Y, mx, my, mz, 2, L.S[2], 1, mz, mz); __syncthreads();
+  for (int w = threadIdx.x; w < Mw; w += blockDim.x) {
+    const int a = w % mx, b = (w / mx) % my, c = w / (mx * my);
+    Y[w] = Y[w] / (L.lam[0][a] + L.lam[1][b] + L.lam[2][c]);
+  }
+  __syncthreads();
+  contract_axis(Y, X, mx, my, mz, 2, L.S[2], mz, 1, mz); __syncthreads();
+  contract_axis(X, Y, mx, my, mz, 1, L.S[1], my, 1, my); __syncthreads();
+  contract_axis(Y, X, mx, my, mz, 0, L.S[0], mx, 1, mx); __syncthreads();
+  double *Ze = Z + (long long)e * Mw;
+  for (int w = threadIdx.x; w < Mw; w += blockDim.x) {
+    const int a = w % mx, b = (w / mx) % my, c = w / (mx * my);
+    Ze[w] = L.W[0][a] * L.W[1][b] * L.W[2][c] * X[w];
+  }
+}
+
+// Deterministic weighted scatter-add (Eq. 10): every DOF pulls the weighted corrections of
+// the (<= 3 per direction) subdomains whose window contains it, in a fixed order; u += du.
+__global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restrict__ u,
+                       int zero) {
+  const int n = L.n, n3 = n * n * n;
+  const int mx = L.m[0], my = L.m[1], Mw = L.Mw;
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int idx[3] = {t % n, (t / n) % n, t / (n * n)};
+    int cnt[3], off[3][3], wi[3][3];
+    for (int d = 0; d < 3; ++d) {
+      const int no = L.no[d], i = idx[d];
+      int c = 0;
+      // subdomain centred on the left neighbour: this node is in its right overlap
+      if (i < no) { off[d][c] = -1; wi[d][c] = no + n + i; ++c; }
+      off[d][c] = 0; wi[d][c] = no + i; ++c;
+      // subdomain centred on the right neighbour: this node is in its left overlap
+      if (i >= n - no) { off[d][c] = 1; wi[d][c] = i - (n - no); ++c; }
+      cnt[d] = c;
+    }
+    double du = 0;
+    for (int cz = 0; cz < cnt[2]; ++cz) {
+      const int sz = wrap(ec[2] + off[2][cz], edim[2]);
+      for (int cy = 0; cy < cnt[1]; ++cy) {
+        const int sy = wrap(ec[1] + off[1][cy], edim[1]);
+        for (int cx = 0; cx < cnt[0]; ++cx) {
+          const int sx = wrap(ec[0] + off[0][cx], edim[0]);
+          const long long s = sx + L.nx * (sy + (long long)L.ny * sz);
+          du += __ldg(Z + s * Mw + wi[0][cx] + mx * (wi[1][cy] + my * wi[2][cz]));
+        }
+      }
+    }
+    const long long g = (long long)e * n3 + t;
+    u[g] = zero ? du : u[g] + du;
+  }
+}
+
+// Residual restriction f_c = I^T r_f per element (Alg. 1 l.292).
+__global__ void k_restrict(int nf, int nc, const double *__restrict__ I,
+                           const double *__restrict__ rf, double *__restrict__ fc) {
+  extern __shared__ double sm[];
+  const int e = blockIdx.x;
+  double *t1 = sm, *t2 = sm + nc * nf * nf;
+  const double *in = rf + (long long)e * nf * nf * nf;
+  contract_axis(in, t1, nf, nf, nf, 0, I, 1, nc, nc); __syncthreads();
+  contract_axis(t1, t2, nc, nf, nf, 1, I, 1, nc, nc); __syncthreads();
+  contract_axis(t2, fc + (long long)e * nc * nc * nc, nc, nc, nf, 2, I, 1, nc, nc);
+}
+
+// Correction prolongation u_f += I u_c per element (Alg. 1 l.299).
+__global__ void k_prolong(int nf, int nc, const double *__restrict__ I,
+                          const double *__restrict__ uc, double *__restrict__ uf) {
+  extern __shared__ double sm[];
+  const int e = blockIdx.x;
+  double *t1 = sm, *t2 = sm + nf * nc * nc;
+  const double *in = uc + (long long)e * nc * nc * nc;
+  contract_axis(in, t1, nc, nc, nc, 0, I, nc, 1, nf); __syncthreads();
+  contract_axis(t1, t2, nf, nc, nc, 1, I, nc, 1, nf); __syncthreads();
+  const int total = nf * nf * nf;
+  double *ue = uf + (long long)e * total;
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int i = t % nf, j = (t / nf) % nf, k = t / (nf * nf);
+    const double *src = t2 + i + nf * j;
+    const double *a = I + k * nc;
+    double acc = 0;
+    for (int c = 0; c < nc; ++c) acc += a[c] * src[c * nf * nf];
+    ue[t] += acc;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Coarse level (P_0 = 1): u_0 = A_0^+ f_0 by global fast diagonalisation on the periodic
+// (2nx, 2ny, 2nz) grid with the constant mode removed (Alg. 1 l.295).
+__global__ void k_coarse_gather(int nx, int ny, int nz, const double *__restrict__ f0,
+                                const double *__restrict__ mean, double *__restrict__ G) {
+  const long long N = 8LL * nx * ny * nz;
+  const double mu = *mean;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int node = g & 7;
+    const long long e = g >> 3;
+    const int i = node & 1, j = (node >> 1) & 1, k = node >> 2;
+    const int ex = e % nx, ey = (e / nx) % ny, ez = e / ((long long)nx * ny);
+    const long long X = 2 * ex + i, Y = 2 * ey + j, Z = 2 * ez + k;
+    G[X + 2LL * nx * (Y + 2LL * ny * Z)] = f0[g] - mu;
+  }
+}
+
+__global__ void k_lex_contract(CoarseDev C, int axis, int forward, const double *__restrict__ in,
+                               double *__restrict__ out) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  const int Gd = C.G[axis];
+  const long long st = axis == 0 ? 1 : (axis == 1 ? C.G[0] : (long long)C.G[0] * C.G[1]);
+  const double *S = C.S[axis];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int o = (g / st) % Gd;
+    const double *src = in + (g - o * st);
+    double acc = 0;
+    if (forward) for (int k = 0; k < Gd; ++k) acc += S[k * Gd + o] * src[k * st];
+    else for (int k = 0; k < Gd; ++k) acc += S[o * Gd + k] * src[k * st];
+    out[g] = acc;
+  }
+}
+
+__global__ void k_coarse_divide(CoarseDev C, double *__restrict__ G) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int a = g % C.G[0], b = (g / C.G[0]) % C.G[1], c = g / ((long long)C.G[0] * C.G[1]);
+    // eigenvalue index 0 is the (exactly zero) constant mode in every direction
+    G[g] = (a == 0 && b == 0 && c == 0) ? 0.0 : G[g] / (C.lam[0][a] + C.lam[1][b] + C.lam[2][c]);
+  }
+}
+
+__global__ void k_coarse_scatter(int nx, int ny, int nz, const double *__restrict__ G,
+                                 const double *__restrict__ mean, double *__restrict__ u0) {
+  const long long N = 8LL * nx * ny * nz;
+  const double mu = *mean;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int node = g & 7;
+    const long long e = g >> 3;
+    const int i = node & 1, j = (node >> 1) & 1, k = node >> 2;
+    const int ex = e % nx, ey = (e / nx) % ny, ez = e / ((long long)nx * ny);
+    const long long X = 2 * ex + i, Y = 2 * ey + j, Z = 2 * ez + k;
+    u0[g] = G[X + 2LL * nx * (Y + 2LL * ny * Z)] - mu;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic reductions: fixed grid for a given N, fixed per-thread order, fixed tree.
+constexpr int RB = 256;
+constexpr int RMAX = 1184;   // 8 x 148 SMs
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[RB / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < RB / 32 ? sh[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  }
+  __syncthreads();
+  return v;   // valid in thread 0
+}
+
+template <int MODE>
+__global__ void k_partial(const double *__restrict__ x, const double *__restrict__ y,
+                          const double *__restrict__ z, long long N, double *__restrict__ part) {
+  // MODE 0: sum x;  1: x.y;  2: (x.(y - z), x.y) two outputs
+  double a = 0, b = 0;
+  for (long long g = blockIdx.x * (long long)RB + threadIdx.x; g < N; g += (long long)gridDim.x * RB) {
+    if (MODE == 0) a += x[g];
+    else if (MODE == 1) a += x[g] * y[g];
+    else { a += x[g] * (y[g] - z[g]); b += x[g] * y[g]; }
+  }
+  a = block_sum(a);
+  if (MODE == 2) b = block_sum(b);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = a;
+    if (MODE == 2) part[gridDim.x + blockIdx.x] = b;
+  }
+}
+
+// final stage: op 0 -> out[0] = scale * sum; op 1 -> pq & alpha; op 2 -> zr / beta
+__global__ void k_final(const double *__restrict__ part, int nb, int nout, double *__restrict__ out,
+                        double scale, int op) {
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < nb; i += RB) {
+    a += part[i];
+    if (nout == 2) b += part[nb + i];
+  }
+  a = block_sum(a);
+  if (nout == 2) b = block_sum(b);
+  if (threadIdx.x == 0) {
+    if (op == 0) out[0] = scale * a;
+    else if (op == 1) { out[1] = a; out[5] = out[0] / a; }                 // pq, alpha = zr/pq
+    else if (op == 2) { out[3] = a; out[4] = b; out[6] = a / out[0]; out[0] = b; }  // beta
+    else if (op == 3) { out[0] = b; }                                        // first zr
+  }
+}
+
+__global__ void k_sub_scalar(double *__restrict__ v, long long N, const double *__restrict__ c) {
+  const double s = *c;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    v[g] -= s;
+}
+
+__global__ void k_copy(double *__restrict__ d, const double *__restrict__ s, long long N) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    d[g] = s ? s[g] : 0.0;
+}
+
+__global__ void k_cg_update(double *__restrict__ u, double *__restrict__ r, double *__restrict__ rold,
+                            const double *__restrict__ p, const double *__restrict__ q, long long N,
+                            double *__restrict__ part, const double *__restrict__ scal) {
+  const double alpha = scal[5];
+  double a = 0;
+  for (long long g = blockIdx.x * (long long)RB + threadIdx.x; g < N; g += (long long)gridDim.x * RB) {
+    u[g] += alpha * p[g];
+    const double ro = r[g];
+    rold[g] = ro;
+    const double rn = ro - alpha * q[g];
+    r[g] = rn;
+    a += rn * rn;
+  }
+  a = block_sum(a);
+  if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+__global__ void k_p_update(double *__restrict__ p, const double *__restrict__ z, long long N,
+                           const double *__restrict__ scal) {
+  const double beta = scal[6];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    p[g] = z[g] + beta * p[g];
+}
+
+// b = M * amp * sin(kx x) sin(ky y) sin(kz z) at the nodes (diagonal quadrature)
+__global__ void k_rhs_sin(LevelDev L, double dx, double dy, double dz, double amp, double kx,
+                          double ky, double kz, double *__restrict__ b) {
+  const int n = L.n, n3 = n * n * n;
+  const long long N = (long long)L.Ne * n3;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long e = g / n3;
+    const int t = g - e * n3;
+    const int i = t % n, j = (t / n) % n, k = t / (n * n);
+    const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / ((long long)L.nx * L.ny);
+    const double x = (ex + 0.5 * (L.nodes[i] + 1.0)) * dx;
+    const double y = (ey + 0.5 * (L.nodes[j] + 1.0)) * dy;
+    const double z = (ez + 0.5 * (L.nodes[k] + 1.0)) * dz;
+    b[g] = L.mass[0][i] * L.mass[1][j] * L.mass[2][k] * amp * sin(kx * x) * sin(ky * y) * sin(kz * z);
+  }
+}
+
+inline int grid_for(long long N, int bs) {
+  long long g = (N + bs - 1) / bs;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s) {
+  k_traces<<<L.Ne, 128, 0, s>>>(L, u, T);
+  return cudaGetLastError();
+}
+cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
+                         double *out, cudaStream_t s) {
+  k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
+                       size_t smem_bytes, cudaStream_t s) {
+  if (smem) {
+    static size_t configured = 0;
+    if (smem_bytes > configured) {
+      cudaFuncSetAttribute(k_fdm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+      configured = smem_bytes;
+    }
+    k_fdm<<<L.Ne, 512, smem_bytes, s>>>(L, r, Z, scr, 1);
+  } else {
+    k_fdm<<<L.Ne, 512, 0, s>>>(L, r, Z, scr, 0);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, cudaStream_t s) {
+  k_fold<<<L.Ne, 256, 0, s>>>(L, Z, u, zero ? 1 : 0);
+  return cudaGetLastError();
+}
+static size_t xfer_smem(int nf, int nc) {
+  return sizeof(double) * ((size_t)nc * nf * nf + (size_t)nc * nc * nf);
+}
+cudaError_t launch_restrict(const LevelDev &Lf, int nc, const double *I, const double *rf,
+                            double *fc, cudaStream_t s) {
+  const size_t sb = xfer_smem(Lf.n, nc);
+  static size_t configured = 0;
+  if (sb > 48 * 1024 && sb > configured) {
+    cudaFuncSetAttribute(k_restrict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    configured = sb;
+  }
+  k_restrict<<<Lf.Ne, 256, sb, s>>>(Lf.n, nc, I, rf, fc);
+  return cudaGetLastError();
+}
+cudaError_t launch_prolong(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                           double *uf, cudaStream_t s) {
+  const size_t sb = xfer_smem(Lf.n, nc);
+  static size_t configured = 0;
+  if (sb > 48 * 1024 && sb > configured) {
+    cudaFuncSetAttribute(k_prolong, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    configured = sb;
+  }
+  k_prolong<<<Lf.Ne, 256, sb, s>>>(Lf.n, nc, I, uc, uf);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarse_gather(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                 const double *mean, double *G, cudaStream_t s) {
+  k_coarse_gather<<<grid_for(8LL * L0.Ne, 256), 256, 0, s>>>(L0.nx, L0.ny, L0.nz, f0, mean, G);
+  return cudaGetLastError();
+}
+cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, const double *in,
+                                double *out, cudaStream_t s) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, axis, forward ? 1 : 0, in, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  k_coarse_divide<<<grid_for(N, 256), 256, 0, s>>>(C, G);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarse_scatter(const LevelDev &L0, const CoarseDev &C, const double *G,
+                                  const double *mean, double *u0, cudaStream_t s) {
+  k_coarse_scatter<<<grid_for(8LL * L0.Ne, 256), 256, 0, s>>>(L0.nx, L0.ny, L0.nz, G, mean, u0);
+  return cudaGetLastError();
+}
+int reduce_blocks(long long N) {
+  long long b = (N + 4 * RB - 1) / (4 * RB);
+  if (b > RMAX) b = RMAX;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+cudaError_t launch_sum(const double *x, long long N, double *partial, double *out, double scale,
+                       cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<0><<<nb, RB, 0, s>>>(x, nullptr, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, out, scale, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot(const double *x, const double *y, long long N, double *partial,
+                       double *out, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<1><<<nb, RB, 0, s>>>(x, y, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, out, 1.0, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_sub_scalar(double *v, long long N, const double *c, cudaStream_t s) {
+  k_sub_scalar<<<grid_for(N, 256), 256, 0, s>>>(v, N, c);
+  return cudaGetLastError();
+}
+cudaError_t launch_copy(double *dst, const double *src, long long N, cudaStream_t s) {
+  k_copy<<<grid_for(N, 256), 256, 0, s>>>(dst, src, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_zero(double *dst, long long N, cudaStream_t s) { return launch_copy(dst, nullptr, N, s); }
+cudaError_t launch_pq_alpha(const double *p, const double *q, long long N, double *partial,
+                            double *scal, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<1><<<nb, RB, 0, s>>>(p, q, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, scal, 1.0, 1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update(double *u, double *r, double *rold, const double *p,
+                             const double *q, long long N, double *partial, double *scal,
+                             cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_cg_update<<<nb, RB, 0, s>>>(u, r, rold, p, q, N, partial, scal);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, scal + 2, 1.0, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_zr_beta(const double *z, const double *r, const double *rold, long long N,
+                           double *partial, double *scal, bool first, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<2><<<nb, RB, 0, s>>>(z, r, rold, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 2, scal, 1.0, first ? 3 : 2);
+  return cudaGetLastError();
+}
+cudaError_t launch_p_update(double *p, const double *z, long long N, const double *scal,
+                            cudaStream_t s) {
+  k_p_update<<<grid_for(N, 256), 256, 0, s>>>(p, z, N, scal);
+  return cudaGetLastError();
+}
+cudaError_t launch_rhs_sin(const LevelDev &L, double dx, double dy, double dz, double amp,
+                           double kx, double ky, double kz, double *b, cudaStream_t s) {
+  k_rhs_sin<<<grid_for((long long)L.Ne * L.n * L.n * L.n, 256), 256, 0, s>>>(L, dx, dy, dz, amp,
+                                                                             kx, ky, kz, b);
+  return cudaGetLastError();
+}
+
+}  // namespace pmg

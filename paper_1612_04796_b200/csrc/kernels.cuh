@@ -1,0 +1,70 @@
+// Device kernels of the p-multigrid V(1,1) hot path (FP64, sm_100a).
+// Paper: arXiv:1612.04796 (PAPER.md line numbers cited per kernel).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace pmg {
+
+// Per-level device view of the setup tables (all pointers into the workspace).
+struct LevelDev {
+  int n, nx, ny, nz, Ne;
+  const double *mass[3];   // (Delta_d/2) w, n each
+  const double *D[3];      // diagonal 1D stiffness block, n*n row-major
+  const double *tr[3];     // 4n: a = phi(+1), ap = (2/D) phi'(+1), b = phi(-1), bp = (2/D) phi'(-1)
+  double mu[3];            // penalty per direction
+  int no[3], m[3];         // overlap layers, window sizes
+  const double *S[3];      // m*m, S[a*m+i] = component a of eigenvector i
+  const double *lam[3];    // m
+  const double *W[3];      // m
+  const double *nodes;     // n reference nodes
+  int Mw;                  // m0*m1*m2
+};
+
+struct CoarseDev {
+  int G[3];                // global 1D sizes 2*n_e
+  const double *S[3];      // G*G row-major (column = eigenvector)
+  const double *lam[3];
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s);
+cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
+                         double *out, cudaStream_t s);
+cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
+                       size_t smem_bytes, cudaStream_t s);
+cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, cudaStream_t s);
+cudaError_t launch_restrict(const LevelDev &Lf, int nc, const double *I, const double *rf,
+                            double *fc, cudaStream_t s);
+cudaError_t launch_prolong(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                           double *uf, cudaStream_t s);
+// coarse solve pieces
+cudaError_t launch_coarse_gather(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                 const double *mean, double *G, cudaStream_t s);
+cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, const double *in,
+                                double *out, cudaStream_t s);
+cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s);
+cudaError_t launch_coarse_scatter(const LevelDev &L0, const CoarseDev &C, const double *G,
+                                  const double *mean, double *u0, cudaStream_t s);
+// reductions (deterministic, two-stage) and vector ops
+int reduce_blocks(long long N);
+cudaError_t launch_sum(const double *x, long long N, double *partial, double *out, double scale,
+                       cudaStream_t s);
+cudaError_t launch_dot(const double *x, const double *y, long long N, double *partial,
+                       double *out, cudaStream_t s);
+cudaError_t launch_sub_scalar(double *v, long long N, const double *c, cudaStream_t s);
+cudaError_t launch_copy(double *dst, const double *src, long long N, cudaStream_t s);
+cudaError_t launch_zero(double *dst, long long N, cudaStream_t s);
+// PCG (Golub-Ye) helpers; scal[] slots documented in api.cu
+cudaError_t launch_pq_alpha(const double *p, const double *q, long long N, double *partial,
+                            double *scal, cudaStream_t s);
+cudaError_t launch_cg_update(double *u, double *r, double *rold, const double *p,
+                             const double *q, long long N, double *partial, double *scal,
+                             cudaStream_t s);
+cudaError_t launch_zr_beta(const double *z, const double *r, const double *rold, long long N,
+                           double *partial, double *scal, bool first, cudaStream_t s);
+cudaError_t launch_p_update(double *p, const double *z, long long N, const double *scal,
+                            cudaStream_t s);
+cudaError_t launch_rhs_sin(const LevelDev &L, double dx, double dy, double dz, double amp,
+                           double kx, double ky, double kz, double *b, cudaStream_t s);
+
+}  // namespace pmg

@@ -1,0 +1,220 @@
+"""GPU-vs-oracle parity (run on a B200 with `pytest -m gpu`), through the C ABI.
+
+Bar (BASELINE.json north_star): relative max-norm error <= 1e-11 for the operator apply and
+one V-cycle's iterate; residual-reduction factor per cycle equal to 3 significant digits.
+Oracle: oracle.mf (validated against the explicit-matrix oracle.dense by the CPU suite) and
+oracle.dense directly on the small grids.  Inputs: workloads (seeded, shared).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from workloads import get_config, uniform_zero_mean, uniform_vector
+from workloads.configs import OverlapSpec, Config
+from oracle.mf import MFHierarchy
+from oracle.dense import DenseHierarchy
+from oracle import mg
+
+TOL = 1e-11
+
+
+def _gpu(c):
+    from paper_1612_04796_b200 import DG
+    return DG(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+
+
+def _t(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+
+
+def _n(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def _rel(a, b):
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+_HCACHE = {}
+
+
+def _oracle(c, dense=False):
+    key = (c.name, c.ne, c.length, c.P, c.basis, c.overlap, dense)
+    if key not in _HCACHE:
+        cls = DenseHierarchy if dense else MFHierarchy
+        _HCACHE[key] = cls(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    return _HCACHE[key]
+
+
+SMALL = [("c1", None), ("c2", 3), ("c3", 3), ("c4", 3), ("c5", 3)]
+FULL = ["c1", "c2", "c4", "c5"]
+
+
+@pytest.mark.parametrize("name,ne", SMALL + [(n, None) for n in FULL[1:]] + [("c3", None)])
+def test_apply_parity(name, ne):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    u = uniform_vector(c.ndofs, 1)
+    Au = _n(g.apply(_t(u)))
+    ref = H.apply(H.L, u)
+    assert _rel(Au, ref) <= TOL
+    # every level's operator
+    for l in range(H.L):
+        ul = uniform_vector(H.ndofs(l), 2)
+        assert _rel(_n(g.apply(_t(ul), level=l)), H.apply(l, ul)) <= TOL
+    f = uniform_zero_mean(c.ndofs, 0)
+    assert _rel(_n(g.residual(_t(u), _t(f))), f - ref) <= TOL
+
+
+@pytest.mark.parametrize("name,ne", [("c1", None), ("c2", 3)])
+def test_apply_parity_dense(name, ne):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c, dense=True)
+    u = uniform_vector(c.ndofs, 1)
+    assert _rel(_n(g.apply(_t(u))), H.apply(H.L, u)) <= TOL
+
+
+@pytest.mark.parametrize("name,ne", SMALL)
+def test_smoother_transfer_coarse_parity(name, ne):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    rng = np.random.default_rng(11)
+    for l in range(1, H.L + 1):
+        u = rng.uniform(-1, 1, H.ndofs(l))
+        f = rng.uniform(-1, 1, H.ndofs(l))
+        ug = _t(u)
+        g.schwarz_smooth(ug, _t(f), steps=2, level=l)
+        assert _rel(_n(ug), H.smooth(l, u, f, 2)) <= TOL, l
+        uc = rng.uniform(-1, 1, H.ndofs(l - 1))
+        ug = _t(u)
+        g.prolongate_add(_t(uc), ug, l)
+        assert _rel(_n(ug), u + H.prolong(l, uc)) <= TOL
+        assert _rel(_n(g.restrict(_t(f), l)), H.restrict(l, f)) <= TOL
+    f0 = rng.uniform(-1, 1, H.ndofs(0))
+    assert _rel(_n(g.coarse_solve(_t(f0))), H.coarse(f0)) <= TOL
+
+
+@pytest.mark.parametrize("name,ne", SMALL + [(n, None) for n in FULL[1:]])
+def test_vcycle_parity(name, ne):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    f = uniform_zero_mean(c.ndofs, 0)
+    u = np.zeros(c.ndofs)
+    ug, fg = _t(u), _t(f)
+    for k in range(2):
+        g.pmg_vcycle(ug, fg)
+        u = mg.vcycle(H, u, f)
+        assert _rel(_n(ug), u) <= TOL, k
+
+
+def test_vcycle_parity_c3_full():
+    test_vcycle_parity("c3", None)
+
+
+@pytest.mark.parametrize("name,ne,cycles", [("c1", None, 12), ("c2", None, 10), ("c4", 3, 6), ("c3", 4, 6)])
+def test_rate_per_cycle_three_digits(name, ne, cycles):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    if c.rhs == "uniform":
+        f = uniform_zero_mean(c.ndofs, 0)
+        fg = _t(f)
+    else:                         # each side assembles its own sin-product RHS (c2)
+        f = _sin_rhs_oracle(c)
+        fg = g.rhs_sin(3.0, 1.0, 1.0, 1.0)
+    ug = torch.zeros_like(fg)
+    u = np.zeros(c.ndofs)
+    r_g, r_o = [np.sqrt(g.dot(fg, fg))], [np.linalg.norm(f)]
+    for k in range(cycles):
+        g.pmg_vcycle(ug, fg)
+        u = mg.vcycle(H, u, f)
+        res = g.residual(ug, fg)
+        r_g.append(np.sqrt(g.dot(res, res)))
+        r_o.append(mg.residual_norm(H, u, f))
+        if r_o[-1] / r_o[0] < 1e-9:
+            break
+    rho_g = np.array(r_g[1:]) / np.array(r_g[:-1])
+    rho_o = np.array(r_o[1:]) / np.array(r_o[:-1])
+    assert np.all(np.abs(rho_g - rho_o) <= 5e-4 * np.abs(rho_o)), (rho_g, rho_o)
+
+
+def _sin_rhs_oracle(c):
+    from oracle.dense import mass_diag, node_coords
+    X, Y, Z = node_coords(c.ne, c.length, c.P, c.basis)
+    b = mass_diag(c.ne, c.length, c.P, c.basis) * 3 * np.sin(X) * np.sin(Y) * np.sin(Z)
+    return b - b.mean()
+
+
+def test_rhs_sin_matches_oracle():
+    c = get_config("c2")
+    g = _gpu(c)
+    b = _sin_rhs_oracle(c)
+    assert np.max(np.abs(_n(g.rhs_sin(3.0, 1.0, 1.0, 1.0)) - b)) <= TOL * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("ne", [3, None])
+def test_pcg_parity_c5(ne):
+    c = get_config("c5", ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    _, hist_g, ok = g.pcg_solve(ug, _t(f), rtol=1e-10, maxit=60)
+    u, hist_o = mg.pcg(H, f, rtol=1e-10, maxit=60)
+    assert ok and len(hist_g) == len(hist_o)
+    # relative residual histories agree to 3 significant digits while above round-off
+    sel = np.array(hist_o) / hist_o[0] >= 1e-9
+    assert np.all(np.abs(hist_g[sel] - np.array(hist_o)[sel]) <= 5e-4 * np.array(hist_o)[sel])
+    assert _rel(_n(ug), u) <= 1e-8      # final iterates (converged to 1e-10 relative residual)
+
+
+# ---- edge cases: minimum grid, P=2, no overlap, full-neighbour overlap, anisotropy
+EDGE = [
+    Config("e-min", (3, 3, 3), (1.0, 1.0, 1.0), 2, 0, OverlapSpec(0, 1, 0)),
+    Config("e-noovl", (3, 4, 5), (1.0, 1.2, 1.5), 4, 1, OverlapSpec(0, 0, 0)),
+    Config("e-full", (3, 3, 4), (1.0, 1.0, 1.3), 4, 0, OverlapSpec(0, 5, 0)),
+    Config("e-gl-half", (4, 3, 3), (2.0, 1.0, 1.0), 8, 1, OverlapSpec(1, 0.5, 0)),
+    Config("e-aniso", (5, 3, 4), (20.0, 1.0, 0.5), 4, 1, OverlapSpec(2, 0.08, 1)),
+]
+
+
+@pytest.mark.parametrize("c", EDGE, ids=[e.name for e in EDGE])
+def test_edge_cases(c):
+    g = _gpu(c)
+    H = MFHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    u = uniform_vector(c.ndofs, 1)
+    assert _rel(_n(g.apply(_t(u))), H.apply(H.L, u)) <= TOL
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    g.pmg_vcycle(ug, _t(f))
+    assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f)) <= TOL
+
+
+def test_determinism_bitwise():
+    c = get_config("c2", 4)
+    g = _gpu(c)
+    f = _t(uniform_zero_mean(c.ndofs, 0))
+    outs = []
+    for _ in range(2):
+        u = torch.zeros_like(f)
+        for _ in range(2):
+            g.pmg_vcycle(u, f)
+        outs.append(_n(u))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_errors_fail_loudly():
+    from paper_1612_04796_b200 import DG, PMGError
+    g = DG((4, 4, 4), (1, 1, 1), 4, 0, overlap=None)
+    u = torch.zeros(g.ndofs(), dtype=torch.float64, device="cuda")
+    with pytest.raises(PMGError):
+        g.pmg_vcycle(u, u)                  # no Schwarz setup / aliased
+    with pytest.raises(PMGError):
+        g.apply(u, out=u)                   # aliased
