@@ -15,8 +15,9 @@ parity and as the timed CPU baseline (BASELINE.md "CPU baseline plan").
   submatrices (Dirichlet truncation, R_s A R_s^T) of the periodic 1D L and M,
   and eigenpairs from mpmath.eigsy at 40 significant digits, then rounded
   (reading R4).
-* Coarse A_0^+: pinned sparse LU of the Kronecker-form A_0, Euclidean
-  projection and re-centring (as O9).
+* Coarse A_0^+: Euclidean projection, global fast diagonalisation of the periodic
+  P=1 Kronecker operator with the zero (constant) mode dropped, Euclidean
+  re-centring (as O9; checked against O-dense's pinned LU and numpy pinv).
 """
 from functools import lru_cache
 import numpy as np
@@ -169,23 +170,32 @@ class MFLevel:
 
 
 class MFCoarse:
+    """A_0^+ f_0 by global fast diagonalisation of the periodic P=1 Kronecker operator
+    (1D eigenpairs at 40 digits; the constant mode has eigenvalue 0 and is dropped) after
+    the Euclidean projection of f_0, then Euclidean re-centring (O9, reading R9).  Pinned
+    against the pinned-LU O-dense coarse solve and numpy.linalg.pinv by tests/."""
+
     def __init__(self, lev):
-        Mx, My, Mz = [sp.diags(m) for m in lev.M1]
-        Lx, Ly, Lz = lev.L1
-        A0 = sp.kron(Mz, sp.kron(My, Lx)) + sp.kron(Mz, sp.kron(Ly, Mx)) + sp.kron(Lz, sp.kron(My, Mx))
-        A0 = sp.csc_matrix(A0)
-        self.N = A0.shape[0]
         self.lev = lev
-        self.lu = spla.splu(A0[1:, 1:].tocsc())
+        self.S, self.lam = [], []
+        for d in range(3):
+            lam, S = restricted_eig(lev.L1[d].toarray(), lev.M1[d])
+            self.S.append(S)
+            self.lam.append(lam)
+        lx, ly, lz = self.lam
+        den = lz[:, None, None] + ly[None, :, None] + lx[None, None, :]
+        null = den <= 1e-12 * den.max()
+        assert null.sum() == 1, "exactly one null mode expected"
+        self.inv = np.where(null, 0.0, 1.0 / np.where(null, 1.0, den))
 
     def solve(self, f0):
         ne, n = self.lev.ne, self.lev.n
-        f = f0 - f0.mean()
-        F = to_lex(f, ne, n).ravel()
-        x = np.zeros(self.N)
-        x[1:] = self.lu.solve(F[1:])
-        x -= x.mean()
-        return from_lex(x.reshape(ne[2] * n, ne[1] * n, ne[0] * n), ne, n)
+        G = to_lex(f0 - f0.mean(), ne, n)
+        Sx, Sy, Sz = self.S
+        T = np.einsum("cba,ai,bj,ck->kji", G, Sx, Sy, Sz, optimize=True) * self.inv
+        X = np.einsum("kji,ai,bj,ck->cba", T, Sx, Sy, Sz, optimize=True)
+        x = from_lex(X, ne, n)
+        return x - x.mean()
 
 
 class MFHierarchy(mg.Hierarchy):

@@ -31,6 +31,7 @@ struct LevelHost {
   size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0;
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
+  ld lam_min[3] = {0, 0, 0}, lam_max[3] = {0, 0, 0};
 };
 
 constexpr size_t FDM_SMEM_MAX = 227 * 1024;
@@ -383,11 +384,17 @@ int dg_schwarz_setup(dg_ctx *c, int mode, double value, int floor_layers) {
       }
       std::vector<ld> lam, Sv;
       pmg::gen_eig(m, Ls, Ms, lam, Sv);
-      if (!(lam[0] > 0)) return fail(c, PMG_ESINGULAR, "restricted operator not regular");
+      h.lam_min[d] = lam[0];
+      h.lam_max[d] = lam[m - 1];
       h.S[d] = to_d(Sv);
       h.lam[d] = to_d(lam);
       h.W[d] = to_d(pmg::hat_weights(h.basis, h.ov[d]));
     }
+    // A_ss regular: every eigenvalue sum lam_x + lam_y + lam_z > 0.  A single
+    // direction may be singular (window = whole periodic line) if another one is not.
+    const ld smin = h.lam_min[0] + h.lam_min[1] + h.lam_min[2];
+    const ld smax = h.lam_max[0] + h.lam_max[1] + h.lam_max[2];
+    if (!(smin > 1e-13L * smax)) return fail(c, PMG_ESINGULAR, "restricted operator A_ss not regular");
   }
   c->schwarz_ready = true;
   c->ovl_mode = mode;

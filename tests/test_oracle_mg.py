@@ -53,6 +53,16 @@ def test_coarse_pseudoinverse(basis):
     assert abs(x.sum()) < 1e-12 * np.abs(x).max() * len(x)
 
 
+@pytest.mark.parametrize("basis", [GLL, GL])
+def test_mf_coarse_matches_dense(basis):
+    ne, length = (3, 4, 5), (1.0, 2.0, 0.5)
+    Hd = DenseHierarchy(ne, length, 2, basis, 2.0, None)
+    Hm = MFHierarchy(ne, length, 2, basis, 2.0, None)
+    f = np.random.default_rng(4).standard_normal(Hd.ndofs(0))
+    a, b = Hd.coarse(f), Hm.coarse(f)
+    assert np.max(np.abs(a - b)) < 1e-12 * np.max(np.abs(a))
+
+
 def test_vcycle_fixed_point():
     c, H = _H("c1", 4)
     u = np.random.default_rng(5).uniform(-1, 1, c.ndofs)
