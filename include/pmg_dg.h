@@ -138,6 +138,10 @@ long long dg_launch_count(const dg_ctx *ctx);
 int dg_profile(dg_ctx *ctx, int enable);
 int dg_profile_read(dg_ctx *ctx, double *ms_out, long long *count_out, int reset);
 
+/* Diagnostic: measured FP64 throughput of this GPU in TFLOP/s with a DFMA (use_dmma = 0) or
+ * DMMA m8n8k4 (use_dmma = 1) saturating kernel on all SMs (the roofline denominator). */
+int pmg_fp64_peak(int use_dmma, double *tflops_out, void *stream);
+
 const char *dg_last_error(const dg_ctx *ctx);
 void dg_destroy(dg_ctx *ctx);
 

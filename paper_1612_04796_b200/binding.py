@@ -41,6 +41,7 @@ _sig = {
     "dg_launch_count": (_ll, [_vp]),
     "dg_profile": (_i, [_vp, _i]),
     "dg_profile_read": (_i, [_vp, _dp, C.POINTER(_ll), _i]),
+    "pmg_fp64_peak": (_i, [_i, _dp, _vp]),
     "dg_last_error": (C.c_char_p, [_vp]),
     "dg_destroy": (None, [_vp]),
 }
@@ -215,6 +216,15 @@ class DG:
             self.close()
         except Exception:
             pass
+
+
+def fp64_peak_tflops(use_dmma=False):
+    """Measured FP64 DFMA (or DMMA) throughput of the current GPU (pmg_fp64_peak)."""
+    v = C.c_double(0)
+    rc = lib.pmg_fp64_peak(1 if use_dmma else 0, C.byref(v), _stream())
+    if rc:
+        raise PMGError(rc, "pmg_fp64_peak failed")
+    return v.value
 
 
 def dg_setup(ne, length, P, basis, penalty=2.0, overlap=None, bind=True):

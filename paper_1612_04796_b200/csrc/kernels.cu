@@ -167,6 +167,185 @@ __global__ void k_fdm(LevelDev L, const double *__restrict__ r, double *__restri
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tensor-core (DMMA m8n8k4 FP64) variant of the subdomain solve.  Each of the six 1D
+// contractions is a small GEMM  C[o, n] = sum_k A[o, k] X[k, n]  with A = S^T (forward) or S
+// (backward), o/k along the contracted direction and n running over the other two directions.
+// The contraction is done IN PLACE in one shared-memory window buffer: a warp owns whole
+// columns n (8 per N-tile), loads all their K values into registers (B fragments), runs the
+// DMMAs, and overwrites the same columns.  A fragments (the m x m eigenvector matrix, zero
+// padded to multiples of 8 x 4) stay in registers for a whole phase.  The eigen-divide is
+// fused into the epilogue of the z-forward phase, the weight W and the store of the weighted
+// window to Z into the epilogue of the x-backward phase.
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+struct WinDims { int m[3]; };
+
+// (o along DIR, n over the two other directions, lower direction fastest) -> window index
+template <int DIR>
+__device__ __forceinline__ void split_n(int n, const int *m, int &p, int &q) {
+  // returns the two "other" coordinates (lower direction first)
+  const int mlow = DIR == 0 ? m[1] : m[0];
+  p = n % mlow;
+  q = n / mlow;
+}
+
+template <int DIR>
+__device__ __forceinline__ int win_index(int o, int p, int q, const int *m) {
+  if (DIR == 0) return o + m[0] * (p + m[1] * q);
+  if (DIR == 1) return p + m[0] * (o + m[1] * q);
+  return p + m[0] * (q + m[1] * o);
+}
+
+// mode 0: plain store; 1: divide by lam_x + lam_y + lam_z; 2: weight and store to global Zg
+template <int DIR, int KS>
+__device__ void fdm_phase(double *X, const double *S, const int *m, bool fwd, int mode,
+                          const double *const *lam, const double *const *W, double *Zg) {
+  constexpr int MT = (KS + 1) / 2;
+  const int md = m[DIR];
+  const int Npts = (m[0] * m[1] * m[2]) / md;
+  const int stride = DIR == 0 ? 1 : (DIR == 1 ? m[0] : m[0] * m[1]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double a[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      a[mt][ks] = (o < md && k < md) ? (fwd ? S[k * md + o] : S[o * md + k]) : 0.0;
+    }
+  const int ntiles = (Npts + 7) >> 3;
+  for (int tile = warp; tile < ntiles; tile += nw) {
+    const int n0 = tile * 8;
+    int p, q;
+    split_n<DIR>(min(n0 + g, Npts - 1), m, p, q);
+    const int bbase = win_index<DIR>(0, p, q, m);
+    double b[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = X[bbase + min(ks * 4 + t, md - 1) * stride];
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], a[mt][ks], b[ks]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = n0 + 2 * t + j;
+      if (n >= Npts) continue;
+      int pj, qj;
+      split_n<DIR>(n, m, pj, qj);
+      const int wbase = win_index<DIR>(0, pj, qj, m);
+      double extra = 0.0, wpq = 1.0;
+      if (mode == 1) {
+        // lam of the two other directions
+        if (DIR == 0) extra = lam[1][pj] + lam[2][qj];
+        else if (DIR == 1) extra = lam[0][pj] + lam[2][qj];
+        else extra = lam[0][pj] + lam[1][qj];
+      } else if (mode == 2) {
+        if (DIR == 0) wpq = W[1][pj] * W[2][qj];
+        else if (DIR == 1) wpq = W[0][pj] * W[2][qj];
+        else wpq = W[0][pj] * W[1][qj];
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o >= md) continue;
+        const int w = wbase + o * stride;
+        double v = c[mt][j];
+        if (mode == 1) v = v * __drcp_rn(extra + lam[DIR][o]);
+        if (mode == 2) Zg[w] = v * (wpq * W[DIR][o]);
+        else X[w] = v;
+      }
+    }
+  }
+}
+
+template <int DIR>
+__device__ void fdm_phase_dispatch(double *X, const double *S, const int *m, bool fwd, int mode,
+                                   const double *const *lam, const double *const *W, double *Zg) {
+  switch ((m[DIR] + 3) >> 2) {
+    case 1: fdm_phase<DIR, 1>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 2: fdm_phase<DIR, 2>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 3: fdm_phase<DIR, 3>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 4: fdm_phase<DIR, 4>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 5: fdm_phase<DIR, 5>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 6: fdm_phase<DIR, 6>(X, S, m, fwd, mode, lam, W, Zg); break;
+    case 7: fdm_phase<DIR, 7>(X, S, m, fwd, mode, lam, W, Zg); break;
+    default: fdm_phase<DIR, 8>(X, S, m, fwd, mode, lam, W, Zg); break;
+  }
+}
+
+// Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
+__global__ void __launch_bounds__(256) k_fdm_mma(LevelDev L, const double *__restrict__ r,
+                                                 double *__restrict__ Z) {
+  extern __shared__ double sm[];
+  const int n = L.n, n3 = n * n * n;
+  const int m[3] = {L.m[0], L.m[1], L.m[2]};
+  const int Mw = L.Mw;
+  double *X = sm;
+  double *Ss[3];
+  const double *lam[3], *W[3];
+  {
+    double *p = sm + Mw;
+    for (int d = 0; d < 3; ++d) { Ss[d] = p; p += m[d] * m[d]; }
+    double *pl = p;
+    for (int d = 0; d < 3; ++d) { lam[d] = pl; pl += m[d]; }
+    double *pw = pl;
+    for (int d = 0; d < 3; ++d) { W[d] = pw; pw += m[d]; }
+  }
+  for (int d = 0; d < 3; ++d) {
+    for (int i = threadIdx.x; i < m[d] * m[d]; i += blockDim.x) Ss[d][i] = L.S[d][i];
+    for (int i = threadIdx.x; i < m[d]; i += blockDim.x) {
+      const_cast<double *>(lam[d])[i] = L.lam[d][i];
+      const_cast<double *>(W[d])[i] = L.W[d][i];
+    }
+  }
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  // gather: one warp per window row (b, c); lanes along a
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = warp; row < m[1] * m[2]; row += nw) {
+    const int b = row % m[1], c = row / m[1];
+    int ely, ly, elz, lz;
+    {
+      const int no = L.no[1];
+      const int o = b < no ? -1 : (b < no + n ? 0 : 1);
+      ly = b < no ? n - no + b : (b < no + n ? b - no : b - no - n);
+      ely = wrap(ec[1] + o, edim[1]);
+    }
+    {
+      const int no = L.no[2];
+      const int o = c < no ? -1 : (c < no + n ? 0 : 1);
+      lz = c < no ? n - no + c : (c < no + n ? c - no : c - no - n);
+      elz = wrap(ec[2] + o, edim[2]);
+    }
+    const long long rowbase = (long long)(L.nx * (ely + L.ny * elz)) * n3 + n * (ly + n * lz);
+    for (int a = lane; a < m[0]; a += 32) {
+      const int no = L.no[0];
+      const int o = a < no ? -1 : (a < no + n ? 0 : 1);
+      const int lx = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
+      const int elx = wrap(ec[0] + o, edim[0]);
+      X[a + m[0] * row] = __ldg(r + rowbase + (long long)elx * n3 + lx);
+    }
+  }
+  __syncthreads();
+  double *Ze = Z + (long long)e * Mw;
+  fdm_phase_dispatch<0>(X, Ss[0], m, true, 0, lam, W, Ze); __syncthreads();
+  fdm_phase_dispatch<1>(X, Ss[1], m, true, 0, lam, W, Ze); __syncthreads();
+  fdm_phase_dispatch<2>(X, Ss[2], m, true, 1, lam, W, Ze); __syncthreads();
+  fdm_phase_dispatch<2>(X, Ss[2], m, false, 0, lam, W, Ze); __syncthreads();
+  fdm_phase_dispatch<1>(X, Ss[1], m, false, 0, lam, W, Ze); __syncthreads();
+  fdm_phase_dispatch<0>(X, Ss[0], m, false, 2, lam, W, Ze);
+}
+
 // Deterministic weighted scatter-add (Eq. 10): every DOF pulls the weighted corrections of
 // the (<= 3 per direction) subdomains whose window contains it, in a fixed order; u += du.
 __global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restrict__ u,
@@ -429,8 +608,28 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
   k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
   return cudaGetLastError();
 }
+size_t fdm_mma_smem_bytes(const LevelDev &L) {
+  size_t d = (size_t)L.Mw;
+  for (int k = 0; k < 3; ++k) d += (size_t)L.m[k] * L.m[k] + 2 * (size_t)L.m[k];
+  return d * sizeof(double);
+}
+
+bool fdm_mma_ok(const LevelDev &L) {
+  return L.m[0] <= 32 && L.m[1] <= 32 && L.m[2] <= 32 && fdm_mma_smem_bytes(L) <= 227 * 1024;
+}
+
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s) {
+  if (fdm_mma_ok(L)) {
+    const size_t sb = fdm_mma_smem_bytes(L);
+    static size_t configured = 0;
+    if (sb > 48 * 1024 && sb > configured) {
+      cudaFuncSetAttribute(k_fdm_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      configured = sb;
+    }
+    k_fdm_mma<<<L.Ne, 256, sb, s>>>(L, r, Z);
+    return cudaGetLastError();
+  }
   if (smem) {
     static size_t configured = 0;
     if (smem_bytes > configured) {
