@@ -13,6 +13,16 @@ namespace {
 
 __device__ __forceinline__ int wrap(int a, int n) { return a < 0 ? a + n : (a >= n ? a - n : a); }
 
+// Asynchronous 8-byte global->shared copies (LDGSTS): many loads in flight per thread.
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void stage(double *dst, const double *src, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) cp_async8(dst + i, src + i);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Face traces (value and normal derivative on both faces of every direction) — the data the
 // rank-2 neighbour couplings of Eq. 7's block-tridiagonal L_* need.
@@ -333,9 +343,10 @@ __global__ void __launch_bounds__(256) k_fdm_mma(LevelDev L, const double *__res
       const int o = a < no ? -1 : (a < no + n ? 0 : 1);
       const int lx = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
       const int elx = wrap(ec[0] + o, edim[0]);
-      X[a + m[0] * row] = __ldg(r + rowbase + (long long)elx * n3 + lx);
+      cp_async8(X + a + m[0] * row, r + rowbase + (long long)elx * n3 + lx);
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   double *Ze = Z + (long long)e * Mw;
   fdm_phase_dispatch<0>(X, Ss[0], m, true, 0, lam, W, Ze); __syncthreads();
@@ -344,6 +355,176 @@ __global__ void __launch_bounds__(256) k_fdm_mma(LevelDev L, const double *__res
   fdm_phase_dispatch<2>(X, Ss[2], m, false, 0, lam, W, Ze); __syncthreads();
   fdm_phase_dispatch<1>(X, Ss[1], m, false, 0, lam, W, Ze); __syncthreads();
   fdm_phase_dispatch<0>(X, Ss[0], m, false, 2, lam, W, Ze);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Shared-memory-staged operator apply with DMMA contractions (Eq. 7).
+// V = Mz My (D_x u) + Mz Mx (D_y u) + My Mx (D_z u) as three small GEMMs over the element's
+// lines (A = D block in registers, B = lines of u in shared memory), then the rank-2 neighbour
+// couplings from the face-trace buffer, then out = v or f - v.
+template <int DIR, int KS>
+__device__ void apply_phase(const double *U, double *V, const double *D, int n,
+                            const double *const *mass) {
+  constexpr int MT = (KS + 1) / 2;
+  const int m[3] = {n, n, n};
+  const int Npts = n * n;
+  const int stride = DIR == 0 ? 1 : (DIR == 1 ? n : n * n);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double a[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      a[mt][ks] = (o < n && k < n) ? D[o * n + k] : 0.0;
+    }
+  const int ntiles = (Npts + 7) >> 3;
+  for (int tile = warp; tile < ntiles; tile += nw) {
+    const int n0 = tile * 8;
+    int p, q;
+    split_n<DIR>(min(n0 + g, Npts - 1), m, p, q);
+    const int bbase = win_index<DIR>(0, p, q, m);
+    double b[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = U[bbase + min(ks * 4 + t, n - 1) * stride];
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], a[mt][ks], b[ks]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int nn = n0 + 2 * t + j;
+      if (nn >= Npts) continue;
+      int pj, qj;
+      split_n<DIR>(nn, m, pj, qj);
+      const int wbase = win_index<DIR>(0, pj, qj, m);
+      double mpq;
+      if (DIR == 0) mpq = mass[1][pj] * mass[2][qj];
+      else if (DIR == 1) mpq = mass[0][pj] * mass[2][qj];
+      else mpq = mass[0][pj] * mass[1][qj];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o >= n) continue;
+        const int w = wbase + o * stride;
+        if (DIR == 0) V[w] = mpq * c[mt][j];
+        else V[w] += mpq * c[mt][j];
+      }
+    }
+  }
+}
+
+template <int DIR>
+__device__ void apply_phase_dispatch(const double *U, double *V, const double *D, int n,
+                                     const double *const *mass) {
+  switch ((n + 3) >> 2) {
+    case 1: apply_phase<DIR, 1>(U, V, D, n, mass); break;
+    case 2: apply_phase<DIR, 2>(U, V, D, n, mass); break;
+    case 3: apply_phase<DIR, 3>(U, V, D, n, mass); break;
+    case 4: apply_phase<DIR, 4>(U, V, D, n, mass); break;
+    default: apply_phase<DIR, 5>(U, V, D, n, mass); break;   // n <= 20
+  }
+}
+
+// smem: U (n^3) | V (n^3) | D_x, D_y, D_z (n^2) | traces 3 x 4n | mass 3 x n
+__global__ void __launch_bounds__(256) k_apply_mma(LevelDev L, const double *__restrict__ u,
+                                                   const double *__restrict__ T,
+                                                   const double *__restrict__ f,
+                                                   double *__restrict__ out) {
+  extern __shared__ double sm[];
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  double *U = sm, *V = sm + n3, *Ds = sm + 2 * n3;
+  double *trs = Ds + 3 * n2, *ms = trs + 12 * n;
+  const int e = blockIdx.x;
+  stage(U, u + (long long)e * n3, n3);
+  for (int d = 0; d < 3; ++d) {
+    stage(Ds + d * n2, L.D[d], n2);
+    stage(trs + d * 4 * n, L.tr[d], 4 * n);
+    stage(ms + d * n, L.mass[d], n);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const double *mass[3] = {ms, ms + n, ms + 2 * n};
+  apply_phase_dispatch<0>(U, V, Ds, n, mass); __syncthreads();
+  apply_phase_dispatch<1>(U, V, Ds + n2, n, mass); __syncthreads();
+  apply_phase_dispatch<2>(U, V, Ds + 2 * n2, n, mass); __syncthreads();
+  // rank-2 neighbour couplings (E+ u_{e+1}, E- u_{e-1}) from the neighbours' face traces,
+  // staged into the (now free) U buffer, or behind the tables when 12 n^2 > n^3:
+  // per direction [tvR | tdR | tvL | tdL] x n^2
+  double *TS = (12 * n2 > n3) ? ms + 3 * n : U;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  const int ecoord[3] = {ex, ey, ez};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  for (int d = 0; d < 3; ++d) {
+    int c[3] = {ex, ey, ez};
+    c[d] = wrap(ecoord[d] + 1, edim[d]);
+    stage(TS + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
+          2 * n2);
+    c[d] = wrap(ecoord[d] - 1, edim[d]);
+    stage(TS + d * 4 * n2 + 2 * n2,
+          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int i = t % n, j = (t / n) % n, k = t / n2;
+    const int idx[3] = {i, j, k};
+    const int pf[3] = {j + n * k, i + n * k, i + n * j};
+    double v = V[t];
+    double s3[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double *tr = trs + d * 4 * n;
+      const int id = idx[d];
+      const double *Tn = TS + d * 4 * n2;
+      const double tvR = Tn[pf[d]], tdR = Tn[n2 + pf[d]];
+      const double tvL = Tn[2 * n2 + pf[d]], tdL = Tn[3 * n2 + pf[d]];
+      const double mu = L.mu[d];
+      s3[d] = tr[id] * (-0.5 * tdR - mu * tvR) + tr[n + id] * (0.5 * tvR)
+            + tr[2 * n + id] * (0.5 * tdL - mu * tvL) + tr[3 * n + id] * (-0.5 * tvL);
+    }
+    v += mass[2][k] * mass[1][j] * s3[0] + mass[2][k] * mass[0][i] * s3[1]
+       + mass[1][j] * mass[0][i] * s3[2];
+    const long long gi = (long long)e * n3 + t;
+    out[gi] = f ? __ldg(f + gi) - v : v;
+  }
+}
+
+// Face traces with the element staged in shared memory (coalesced loads).
+__global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__restrict__ u,
+                                                   double *__restrict__ T) {
+  extern __shared__ double sm[];
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  double *U = sm, *trs = sm + n3;
+  const int e = blockIdx.x;
+  stage(U, u + (long long)e * n3, n3);
+  for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
+  cp_async_wait_all();
+  __syncthreads();
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = U[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
 }
 
 // Deterministic weighted scatter-add (Eq. 10): every DOF pulls the weighted corrections of
@@ -600,12 +781,35 @@ inline int grid_for(long long N, int bs) {
 
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s) {
-  k_traces<<<L.Ne, 128, 0, s>>>(L, u, T);
+  const int n = L.n;
+  const size_t sb = sizeof(double) * ((size_t)n * n * n + 12 * n);
+  if (n <= 20) {
+    static size_t configured = 0;
+    if (sb > 48 * 1024 && sb > configured) {
+      cudaFuncSetAttribute(k_traces_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      configured = sb;
+    }
+    k_traces_sm<<<L.Ne, 256, sb, s>>>(L, u, T);
+  } else {
+    k_traces<<<L.Ne, 128, 0, s>>>(L, u, T);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
                          double *out, cudaStream_t s) {
-  k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
+  const int n = L.n;
+  if (n <= 20) {
+    const size_t n2 = (size_t)n * n, n3 = n2 * n;
+    const size_t sb = sizeof(double) * (2 * n3 + 3 * n2 + 15 * n + (12 * n2 > n3 ? 12 * n2 : 0));
+    static size_t configured = 0;
+    if (sb > 48 * 1024 && sb > configured) {
+      cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      configured = sb;
+    }
+    k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out);
+  } else {
+    k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
+  }
   return cudaGetLastError();
 }
 size_t fdm_mma_smem_bytes(const LevelDev &L) {
