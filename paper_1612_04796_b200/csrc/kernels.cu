@@ -178,46 +178,44 @@ __global__ void k_fdm(LevelDev L, const double *__restrict__ r, double *__restri
 }
 
 // ---------------------------------------------------------------------------------------------
-// Tensor-core (DMMA m8n8k4 FP64) variant of the subdomain solve.  Each of the six 1D
-// contractions is a small GEMM  C[o, n] = sum_k A[o, k] X[k, n]  with A = S^T (forward) or S
-// (backward), o/k along the contracted direction and n running over the other two directions.
-// The contraction is done IN PLACE in one shared-memory window buffer: a warp owns whole
-// columns n (8 per N-tile), loads all their K values into registers (B fragments), runs the
-// DMMAs, and overwrites the same columns.  A fragments (the m x m eigenvector matrix, zero
-// padded to multiples of 8 x 4) stay in registers for a whole phase.  The eigen-divide is
-// fused into the epilogue of the z-forward phase, the weight W and the store of the weighted
-// window to Z into the epilogue of the x-backward phase.
+// Tensor-core (DMMA m8n8k4 FP64) line contractions.  Every 1D contraction of the hot path
+// (the six fast-diagonalisation passes and the three stiffness passes of the apply) is a small
+// GEMM  C[o, (p,q)] = sum_k A[o, k] X[k along DIR, p, q]  over a 3D block in shared memory:
+// A (the m x m eigenvector or stiffness matrix, zero padded to 8 x 4 multiples) stays in
+// registers for the whole pass; a warp owns pairs of 8-column N-tiles (columns = 8 consecutive
+// p at fixed q, so no per-lane index division), loads their K values (B fragments), issues
+// MT x KS DMMAs per tile with 2*MT independent accumulator chains, and hands every result to
+// an epilogue policy (store in place, divide by the eigenvalue sum, weight + store to global,
+// or mass-weighted accumulation for the apply).
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-struct WinDims { int m[3]; };
+struct Blk { int m[3]; int s[3]; };   // sizes and shared-memory strides (s[0] = 1)
 
-// (o along DIR, n over the two other directions, lower direction fastest) -> window index
-template <int DIR>
-__device__ __forceinline__ void split_n(int n, const int *m, int &p, int &q) {
-  // returns the two "other" coordinates (lower direction first)
-  const int mlow = DIR == 0 ? m[1] : m[0];
-  p = n % mlow;
-  q = n / mlow;
+// 1/x for x > 0: MUFU reciprocal seed + two Newton steps (relative error ~1 ulp)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
-template <int DIR>
-__device__ __forceinline__ int win_index(int o, int p, int q, const int *m) {
-  if (DIR == 0) return o + m[0] * (p + m[1] * q);
-  if (DIR == 1) return p + m[0] * (o + m[1] * q);
-  return p + m[0] * (q + m[1] * o);
-}
+template <int DIR> struct Other {
+  static constexpr int P = DIR == 0 ? 1 : 0;   // lower of the two other directions
+  static constexpr int Q = DIR == 2 ? 1 : 2;   // higher
+};
 
-// mode 0: plain store; 1: divide by lam_x + lam_y + lam_z; 2: weight and store to global Zg
-template <int DIR, int KS>
-__device__ void fdm_phase(double *X, const double *S, const int *m, bool fwd, int mode,
-                          const double *const *lam, const double *const *W, double *Zg) {
+template <int DIR, int KS, class Epi>
+__device__ __forceinline__ void mma_lines(const double *X, const Blk &B, const double *Amat, int ao,
+                                          int ak, Epi &epi) {
   constexpr int MT = (KS + 1) / 2;
-  const int md = m[DIR];
-  const int Npts = (m[0] * m[1] * m[2]) / md;
-  const int stride = DIR == 0 ? 1 : (DIR == 1 ? m[0] : m[0] * m[1]);
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  const int md = B.m[DIR], mp = B.m[PD], mq = B.m[QD];
+  const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   double a[MT][KS];
@@ -226,74 +224,121 @@ __device__ void fdm_phase(double *X, const double *S, const int *m, bool fwd, in
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int o = mt * 8 + g, k = ks * 4 + t;
-      a[mt][ks] = (o < md && k < md) ? (fwd ? S[k * md + o] : S[o * md + k]) : 0.0;
+      a[mt][ks] = (o < md && k < md) ? Amat[o * ao + k * ak] : 0.0;
     }
-  const int ntiles = (Npts + 7) >> 3;
-  for (int tile = warp; tile < ntiles; tile += nw) {
-    const int n0 = tile * 8;
-    int p, q;
-    split_n<DIR>(min(n0 + g, Npts - 1), m, p, q);
-    const int bbase = win_index<DIR>(0, p, q, m);
-    double b[KS];
+  int koff[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) b[ks] = X[bbase + min(ks * 4 + t, md - 1) * stride];
-    double c[MT][2];
+  for (int ks = 0; ks < KS; ++ks) koff[ks] = min(ks * 4 + t, md - 1) * so;
+  const int ptiles = (mp + 7) >> 3;
+  const int ntiles = ptiles * mq;
+  for (int tile = 2 * warp; tile < ntiles; tile += 2 * nw) {
+    int p0[2], q[2];
+    bool valid[2];
+    double b[2][KS];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+    for (int u = 0; u < 2; ++u) {
+      const int tl = tile + u;
+      valid[u] = tl < ntiles;
+      const int tt = valid[u] ? tl : tile;
+      q[u] = tt / ptiles;
+      p0[u] = (tt - q[u] * ptiles) * 8;
+      const int base = min(p0[u] + g, mp - 1) * sp + q[u] * sq;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) b[u][ks] = X[base + koff[ks]];
+    }
+    double c[2][MT][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) { c[u][mt][0] = 0.0; c[u][mt][1] = 0.0; }
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], a[mt][ks], b[ks]);
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma884(c[u][mt][0], c[u][mt][1], a[mt][ks], b[u][ks]);
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int n = n0 + 2 * t + j;
-      if (n >= Npts) continue;
-      int pj, qj;
-      split_n<DIR>(n, m, pj, qj);
-      const int wbase = win_index<DIR>(0, pj, qj, m);
-      double extra = 0.0, wpq = 1.0;
-      if (mode == 1) {
-        // lam of the two other directions
-        if (DIR == 0) extra = lam[1][pj] + lam[2][qj];
-        else if (DIR == 1) extra = lam[0][pj] + lam[2][qj];
-        else extra = lam[0][pj] + lam[1][qj];
-      } else if (mode == 2) {
-        if (DIR == 0) wpq = W[1][pj] * W[2][qj];
-        else if (DIR == 1) wpq = W[0][pj] * W[2][qj];
-        else wpq = W[0][pj] * W[1][qj];
-      }
+    for (int u = 0; u < 2; ++u) {
+      if (!valid[u]) continue;
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int o = mt * 8 + g;
-        if (o >= md) continue;
-        const int w = wbase + o * stride;
-        double v = c[mt][j];
-        if (mode == 1) v = v * __drcp_rn(extra + lam[DIR][o]);
-        if (mode == 2) Zg[w] = v * (wpq * W[DIR][o]);
-        else X[w] = v;
+      for (int j = 0; j < 2; ++j) {
+        const int p = p0[u] + 2 * t + j;
+        if (p >= mp) continue;
+        const double cf = epi.template col<DIR>(p, q[u]);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int o = mt * 8 + g;
+          if (o < md) epi.template put<DIR>(o, p, q[u], cf, c[u][mt][j]);
+        }
       }
     }
+  }
+}
+
+template <int DIR, class Epi>
+__device__ void mma_lines_dispatch(const double *X, const Blk &B, const double *Amat, int ao,
+                                   int ak, Epi &epi) {
+  switch ((B.m[DIR] + 3) >> 2) {
+    case 1: mma_lines<DIR, 1>(X, B, Amat, ao, ak, epi); break;
+    case 2: mma_lines<DIR, 2>(X, B, Amat, ao, ak, epi); break;
+    case 3: mma_lines<DIR, 3>(X, B, Amat, ao, ak, epi); break;
+    case 4: mma_lines<DIR, 4>(X, B, Amat, ao, ak, epi); break;
+    case 5: mma_lines<DIR, 5>(X, B, Amat, ao, ak, epi); break;
+    case 6: mma_lines<DIR, 6>(X, B, Amat, ao, ak, epi); break;
+    case 7: mma_lines<DIR, 7>(X, B, Amat, ao, ak, epi); break;
+    default: mma_lines<DIR, 8>(X, B, Amat, ao, ak, epi); break;
   }
 }
 
 template <int DIR>
-__device__ void fdm_phase_dispatch(double *X, const double *S, const int *m, bool fwd, int mode,
-                                   const double *const *lam, const double *const *W, double *Zg) {
-  switch ((m[DIR] + 3) >> 2) {
-    case 1: fdm_phase<DIR, 1>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 2: fdm_phase<DIR, 2>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 3: fdm_phase<DIR, 3>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 4: fdm_phase<DIR, 4>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 5: fdm_phase<DIR, 5>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 6: fdm_phase<DIR, 6>(X, S, m, fwd, mode, lam, W, Zg); break;
-    case 7: fdm_phase<DIR, 7>(X, S, m, fwd, mode, lam, W, Zg); break;
-    default: fdm_phase<DIR, 8>(X, S, m, fwd, mode, lam, W, Zg); break;
-  }
+__device__ __forceinline__ int blk_index(const Blk &B, int o, int p, int q) {
+  return o * B.s[DIR] + p * B.s[Other<DIR>::P] + q * B.s[Other<DIR>::Q];
 }
 
+// in-place store
+struct EpiStore {
+  double *X; Blk B;
+  template <int DIR> __device__ __forceinline__ double col(int, int) const { return 0.0; }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double, double v) const {
+    X[blk_index<DIR>(B, o, p, q)] = v;
+  }
+};
+// in-place store divided by lam_x + lam_y + lam_z (fast-diagonalisation divide)
+struct EpiDivide {
+  double *X; Blk B; const double *lam[3];
+  template <int DIR> __device__ __forceinline__ double col(int p, int q) const {
+    return lam[Other<DIR>::P][p] + lam[Other<DIR>::Q][q];
+  }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
+    X[blk_index<DIR>(B, o, p, q)] = v * rcp_nr(cf + lam[DIR][o]);
+  }
+};
+// weight W_x W_y W_z and store the window to global memory (unpadded window order)
+struct EpiWeightStore {
+  double *Zg; Blk G; const double *W[3];
+  template <int DIR> __device__ __forceinline__ double col(int p, int q) const {
+    return W[Other<DIR>::P][p] * W[Other<DIR>::Q][q];
+  }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
+    Zg[blk_index<DIR>(G, o, p, q)] = v * (cf * W[DIR][o]);
+  }
+};
+// mass-weighted accumulation of one term of Eq. 7 into V
+struct EpiMassAcc {
+  double *V; Blk B; const double *mass[3]; bool first;
+  template <int DIR> __device__ __forceinline__ double col(int p, int q) const {
+    return mass[Other<DIR>::P][p] * mass[Other<DIR>::Q][q];
+  }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
+    const int w = blk_index<DIR>(B, o, p, q);
+    if (first) V[w] = cf * v;
+    else V[w] += cf * v;
+  }
+};
+
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
-__global__ void __launch_bounds__(256) k_fdm_mma(LevelDev L, const double *__restrict__ r,
+__global__ void __launch_bounds__(256, 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
                                                  double *__restrict__ Z) {
   extern __shared__ double sm[];
   const int n = L.n, n3 = n * n * n;
@@ -301,133 +346,66 @@ __global__ void __launch_bounds__(256) k_fdm_mma(LevelDev L, const double *__res
   const int Mw = L.Mw;
   double *X = sm;
   double *Ss[3];
-  const double *lam[3], *W[3];
+  double *lam[3], *W[3];
   {
     double *p = sm + Mw;
     for (int d = 0; d < 3; ++d) { Ss[d] = p; p += m[d] * m[d]; }
-    double *pl = p;
-    for (int d = 0; d < 3; ++d) { lam[d] = pl; pl += m[d]; }
-    double *pw = pl;
-    for (int d = 0; d < 3; ++d) { W[d] = pw; pw += m[d]; }
+    for (int d = 0; d < 3; ++d) { lam[d] = p; p += m[d]; }
+    for (int d = 0; d < 3; ++d) { W[d] = p; p += m[d]; }
   }
   for (int d = 0; d < 3; ++d) {
-    for (int i = threadIdx.x; i < m[d] * m[d]; i += blockDim.x) Ss[d][i] = L.S[d][i];
-    for (int i = threadIdx.x; i < m[d]; i += blockDim.x) {
-      const_cast<double *>(lam[d])[i] = L.lam[d][i];
-      const_cast<double *>(W[d])[i] = L.W[d][i];
-    }
+    stage(Ss[d], L.S[d], m[d] * m[d]);
+    stage(lam[d], L.lam[d], m[d]);
+    stage(W[d], L.W[d], m[d]);
   }
   const int e = blockIdx.x;
   const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
   const int edim[3] = {L.nx, L.ny, L.nz};
-  // gather: one warp per window row (b, c); lanes along a
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int row = warp; row < m[1] * m[2]; row += nw) {
-    const int b = row % m[1], c = row / m[1];
-    int ely, ly, elz, lz;
-    {
-      const int no = L.no[1];
-      const int o = b < no ? -1 : (b < no + n ? 0 : 1);
-      ly = b < no ? n - no + b : (b < no + n ? b - no : b - no - n);
-      ely = wrap(ec[1] + o, edim[1]);
+  // gather offsets: global address of window node (a, b, c) = xoff[a] + yoff[b] + zoff[c]
+  long long *offs = reinterpret_cast<long long *>(W[2] + m[2]);
+  {
+    const long long estride[3] = {(long long)n3, (long long)L.nx * n3, (long long)L.nx * L.ny * n3};
+    const int lstride[3] = {1, n, n * n};
+    int base = 0;
+    for (int d = 0; d < 3; ++d) {
+      const int no = L.no[d];
+      for (int a = threadIdx.x; a < m[d]; a += blockDim.x) {
+        const int o = a < no ? -1 : (a < no + n ? 0 : 1);
+        const int li = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
+        offs[base + a] = wrap(ec[d] + o, edim[d]) * estride[d] + li * lstride[d];
+      }
+      base += m[d];
     }
-    {
-      const int no = L.no[2];
-      const int o = c < no ? -1 : (c < no + n ? 0 : 1);
-      lz = c < no ? n - no + c : (c < no + n ? c - no : c - no - n);
-      elz = wrap(ec[2] + o, edim[2]);
-    }
-    const long long rowbase = (long long)(L.nx * (ely + L.ny * elz)) * n3 + n * (ly + n * lz);
-    for (int a = lane; a < m[0]; a += 32) {
-      const int no = L.no[0];
-      const int o = a < no ? -1 : (a < no + n ? 0 : 1);
-      const int lx = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
-      const int elx = wrap(ec[0] + o, edim[0]);
-      cp_async8(X + a + m[0] * row, r + rowbase + (long long)elx * n3 + lx);
+  }
+  __syncthreads();
+  {
+    const long long *xo = offs, *yo = offs + m[0], *zo = offs + m[0] + m[1];
+    const int total = m[0] * m[1] * m[2];
+    // thread-linear over the window: coalesced-ish global reads, contiguous smem writes
+    int a = threadIdx.x % m[0], bc = threadIdx.x / m[0];
+    int b = bc % m[1], c = bc / m[1];
+    const int da = blockDim.x % m[0], dbc = blockDim.x / m[0];
+    for (int w = threadIdx.x; w < total; w += blockDim.x) {
+      cp_async8(X + w, r + xo[a] + yo[b] + zo[c]);
+      a += da; b += dbc;
+      if (a >= m[0]) { a -= m[0]; ++b; }
+      while (b >= m[1]) { b -= m[1]; ++c; }
     }
   }
   cp_async_wait_all();
   __syncthreads();
-  double *Ze = Z + (long long)e * Mw;
-  fdm_phase_dispatch<0>(X, Ss[0], m, true, 0, lam, W, Ze); __syncthreads();
-  fdm_phase_dispatch<1>(X, Ss[1], m, true, 0, lam, W, Ze); __syncthreads();
-  fdm_phase_dispatch<2>(X, Ss[2], m, true, 1, lam, W, Ze); __syncthreads();
-  fdm_phase_dispatch<2>(X, Ss[2], m, false, 0, lam, W, Ze); __syncthreads();
-  fdm_phase_dispatch<1>(X, Ss[1], m, false, 0, lam, W, Ze); __syncthreads();
-  fdm_phase_dispatch<0>(X, Ss[0], m, false, 2, lam, W, Ze);
-}
-
-// ---------------------------------------------------------------------------------------------
-// Shared-memory-staged operator apply with DMMA contractions (Eq. 7).
-// V = Mz My (D_x u) + Mz Mx (D_y u) + My Mx (D_z u) as three small GEMMs over the element's
-// lines (A = D block in registers, B = lines of u in shared memory), then the rank-2 neighbour
-// couplings from the face-trace buffer, then out = v or f - v.
-template <int DIR, int KS>
-__device__ void apply_phase(const double *U, double *V, const double *D, int n,
-                            const double *const *mass) {
-  constexpr int MT = (KS + 1) / 2;
-  const int m[3] = {n, n, n};
-  const int Npts = n * n;
-  const int stride = DIR == 0 ? 1 : (DIR == 1 ? n : n * n);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  double a[MT][KS];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int o = mt * 8 + g, k = ks * 4 + t;
-      a[mt][ks] = (o < n && k < n) ? D[o * n + k] : 0.0;
-    }
-  const int ntiles = (Npts + 7) >> 3;
-  for (int tile = warp; tile < ntiles; tile += nw) {
-    const int n0 = tile * 8;
-    int p, q;
-    split_n<DIR>(min(n0 + g, Npts - 1), m, p, q);
-    const int bbase = win_index<DIR>(0, p, q, m);
-    double b[KS];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) b[ks] = U[bbase + min(ks * 4 + t, n - 1) * stride];
-    double c[MT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], a[mt][ks], b[ks]);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int nn = n0 + 2 * t + j;
-      if (nn >= Npts) continue;
-      int pj, qj;
-      split_n<DIR>(nn, m, pj, qj);
-      const int wbase = win_index<DIR>(0, pj, qj, m);
-      double mpq;
-      if (DIR == 0) mpq = mass[1][pj] * mass[2][qj];
-      else if (DIR == 1) mpq = mass[0][pj] * mass[2][qj];
-      else mpq = mass[0][pj] * mass[1][qj];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int o = mt * 8 + g;
-        if (o >= n) continue;
-        const int w = wbase + o * stride;
-        if (DIR == 0) V[w] = mpq * c[mt][j];
-        else V[w] += mpq * c[mt][j];
-      }
-    }
-  }
-}
-
-template <int DIR>
-__device__ void apply_phase_dispatch(const double *U, double *V, const double *D, int n,
-                                     const double *const *mass) {
-  switch ((n + 3) >> 2) {
-    case 1: apply_phase<DIR, 1>(U, V, D, n, mass); break;
-    case 2: apply_phase<DIR, 2>(U, V, D, n, mass); break;
-    case 3: apply_phase<DIR, 3>(U, V, D, n, mass); break;
-    case 4: apply_phase<DIR, 4>(U, V, D, n, mass); break;
-    default: apply_phase<DIR, 5>(U, V, D, n, mass); break;   // n <= 20
-  }
+  const Blk B = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};
+  EpiStore st{X, B};
+  EpiDivide dv{X, B, {lam[0], lam[1], lam[2]}};
+  EpiWeightStore ws{Z + (long long)e * Mw, B, {W[0], W[1], W[2]}};
+  // forward: A = S^T, i.e. A[o][k] = S[k*m + o]
+  mma_lines_dispatch<0>(X, B, Ss[0], 1, m[0], st); __syncthreads();
+  mma_lines_dispatch<1>(X, B, Ss[1], 1, m[1], st); __syncthreads();
+  mma_lines_dispatch<2>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
+  // backward: A = S
+  mma_lines_dispatch<2>(X, B, Ss[2], m[2], 1, st); __syncthreads();
+  mma_lines_dispatch<1>(X, B, Ss[1], m[1], 1, st); __syncthreads();
+  mma_lines_dispatch<0>(X, B, Ss[0], m[0], 1, ws);
 }
 
 // smem: U (n^3) | V (n^3) | D_x, D_y, D_z (n^2) | traces 3 x 4n | mass 3 x n
@@ -449,9 +427,12 @@ __global__ void __launch_bounds__(256) k_apply_mma(LevelDev L, const double *__r
   cp_async_wait_all();
   __syncthreads();
   const double *mass[3] = {ms, ms + n, ms + 2 * n};
-  apply_phase_dispatch<0>(U, V, Ds, n, mass); __syncthreads();
-  apply_phase_dispatch<1>(U, V, Ds + n2, n, mass); __syncthreads();
-  apply_phase_dispatch<2>(U, V, Ds + 2 * n2, n, mass); __syncthreads();
+  const Blk B = {{n, n, n}, {1, n, n2}};
+  EpiMassAcc acc{V, B, {mass[0], mass[1], mass[2]}, true};
+  mma_lines_dispatch<0>(U, B, Ds, n, 1, acc); __syncthreads();
+  acc.first = false;
+  mma_lines_dispatch<1>(U, B, Ds + n2, n, 1, acc); __syncthreads();
+  mma_lines_dispatch<2>(U, B, Ds + 2 * n2, n, 1, acc); __syncthreads();
   // rank-2 neighbour couplings (E+ u_{e+1}, E- u_{e-1}) from the neighbours' face traces,
   // staged into the (now free) U buffer, or behind the tables when 12 n^2 > n^3:
   // per direction [tvR | tdR | tvL | tdL] x n^2
@@ -814,7 +795,7 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
 }
 size_t fdm_mma_smem_bytes(const LevelDev &L) {
   size_t d = (size_t)L.Mw;
-  for (int k = 0; k < 3; ++k) d += (size_t)L.m[k] * L.m[k] + 2 * (size_t)L.m[k];
+  for (int k = 0; k < 3; ++k) d += (size_t)L.m[k] * L.m[k] + 3 * (size_t)L.m[k];   // S, lam, W, offsets
   return d * sizeof(double);
 }
 
