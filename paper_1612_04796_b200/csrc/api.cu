@@ -25,9 +25,9 @@ struct LevelHost {
   pmg::Overlap1D ov[3];
   int m[3] = {0, 0, 0};
   int Mw = 0;
-  std::vector<double> mass[3], D[3], tr[3], S[3], lam[3], W[3], interp, nodes;
+  std::vector<double> mass[3], D[3], tr[3], S[3], lam[3], W[3], interp, nodes, Daug[3];
   // workspace byte offsets
-  size_t o_mass[3], o_D[3], o_tr[3], o_S[3], o_lam[3], o_W[3], o_interp = 0, o_nodes = 0;
+  size_t o_mass[3], o_D[3], o_tr[3], o_S[3], o_lam[3], o_W[3], o_Daug[3], o_interp = 0, o_nodes = 0;
   size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0;
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
@@ -98,6 +98,7 @@ pmg::LevelDev level_dev(const dg_ctx *c, int l) {
     d.S[k] = h.S[k].empty() ? nullptr : wsp<double>(c, h.o_S[k]);
     d.lam[k] = h.lam[k].empty() ? nullptr : wsp<double>(c, h.o_lam[k]);
     d.W[k] = h.W[k].empty() ? nullptr : wsp<double>(c, h.o_W[k]);
+    d.Daug[k] = wsp<double>(c, h.o_Daug[k]);
   }
   d.nodes = wsp<double>(c, h.o_nodes);
   d.Mw = h.Mw;
@@ -138,6 +139,7 @@ void plan_workspace(dg_ctx *c) {
       h.o_S[d] = p.dbl(h.S[d].size());
       h.o_lam[d] = p.dbl(h.lam[d].size());
       h.o_W[d] = p.dbl(h.W[d].size());
+      h.o_Daug[d] = p.dbl(h.Daug[d].size());
     }
     h.o_interp = p.dbl(h.interp.size());
     h.o_nodes = p.dbl(n);
@@ -204,32 +206,38 @@ int check_level(dg_ctx *c, int level, bool need_ws = true) {
   return PMG_OK;
 }
 
-// r = f - A u (f == nullptr: r = A u)
-int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *out, cudaStream_t s) {
+// r = f - A u (f == nullptr: r = A u).  have_traces: T_l already holds the traces of u
+// (written by the fused fold kernel that produced u in this same cycle).
+int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *out, cudaStream_t s,
+                  bool have_traces = false) {
   pmg::LevelDev d = level_dev(c, l);
   double *T = wsp<double>(c, c->lev[l].o_T);
-  LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
+  if (!have_traces) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
   LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply(d, u, T, f, out, s));
   return PMG_OK;
 }
 
+// `steps` Schwarz iterations.  traces_after: the last fold also emits the traces of the final u
+// (the caller's next operation is a residual of u on this level).
 int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool zero_init,
-                cudaStream_t s) {
+                cudaStream_t s, bool traces_after = false) {
   LevelHost &h = c->lev[l];
   pmg::LevelDev d = level_dev(c, l);
   double *r = wsp<double>(c, h.o_r);
   double *Z = wsp<double>(c, h.o_Z);
+  double *T = wsp<double>(c, h.o_T);
   double *scr = h.o_scr ? wsp<double>(c, h.o_scr) : nullptr;
   for (int it = 0; it < steps; ++it) {
     const bool zero = zero_init && it == 0;
     const double *rin = f;                       // u == 0  =>  r = f (Alg. 1 l.287-290)
     if (!zero) {
-      int st = residual_impl(c, l, u, f, r, s);
+      int st = residual_impl(c, l, u, f, r, s, it > 0);
       if (st) return st;
       rin = r;
     }
     LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
-    LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, s));
+    const bool emit = (it + 1 < steps) || traces_after;
+    LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, emit ? T : nullptr, s));
   }
   if (steps == 0 && zero_init) LAUNCH(c, pmg::launch_zero(u, h.N, s));
   return PMG_OK;
@@ -269,9 +277,10 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
   int st;
   for (int l = L; l >= 1; --l) {                                  // l.286
     const bool zero = (l < L) || zero_top;                         // l.287-289
-    if ((st = smooth_impl(c, l, U[l], F[l], c->nu1[l], zero, s))) return st;   // l.290
+    const int nu = c->nu1[l];
+    if ((st = smooth_impl(c, l, U[l], F[l], nu, zero, s, true))) return st;   // l.290
     double *r = wsp<double>(c, c->lev[l].o_r);
-    if ((st = residual_impl(c, l, U[l], F[l], r, s))) return st;  // l.292
+    if ((st = residual_impl(c, l, U[l], F[l], r, s, nu > 0))) return st;      // l.292
     pmg::LevelDev d = level_dev(c, l);
     LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n, wsp<double>(c, c->lev[l].o_interp), r,
                                    F[l - 1], s));
@@ -325,6 +334,17 @@ int dg_setup(int nx, int ny, int nz, double lx, double ly, double lz, int P, int
         for (int i = 0; i < h.n; ++i) h.mass[d][i] = (double)h.op[d].M[i];
         h.D[d] = to_d(h.op[d].Dblk);
         h.tr[d] = to_d(h.op[d].tr);
+        // augmented stiffness [D | a ap b bp] (n x (n+4)): the rank-2 neighbour couplings
+        // become four extra K columns of the apply's line GEMM
+        // rows pre-scaled by 1/M_d[o]: A u = M (x) (sum_d M_d^-1 L_d u), so the three line
+        // GEMMs accumulate without per-direction mass factors and one M multiply finishes
+        h.Daug[d].assign(h.n * (h.n + 4), 0.0);
+        for (int o = 0; o < h.n; ++o) {
+          const ld im = 1 / h.op[d].M[o];
+          for (int k = 0; k < h.n; ++k) h.Daug[d][o * (h.n + 4) + k] = (double)(h.op[d].Dblk[o * h.n + k] * im);
+          for (int r = 0; r < 4; ++r)
+            h.Daug[d][o * (h.n + 4) + h.n + r] = (double)(h.op[d].tr[r * h.n + o] * im);
+        }
         h.m[d] = h.n;
       }
       if (l >= 1) h.interp = to_d(pmg::interp_matrix(c->lev[l - 1].basis, h.basis));
@@ -460,6 +480,7 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
       if (e == cudaSuccess) e = up(h.o_S[d], h.S[d]);
       if (e == cudaSuccess) e = up(h.o_lam[d], h.lam[d]);
       if (e == cudaSuccess) e = up(h.o_W[d], h.W[d]);
+      if (e == cudaSuccess) e = up(h.o_Daug[d], h.Daug[d]);
     }
     if (e == cudaSuccess) e = up(h.o_interp, h.interp);
     if (e == cudaSuccess) e = up(h.o_nodes, h.nodes);

@@ -209,12 +209,22 @@ template <int DIR> struct Other {
   static constexpr int Q = DIR == 2 ? 1 : 2;   // higher
 };
 
-template <int DIR, int KS, class Epi>
-__device__ __forceinline__ void mma_lines(const double *X, const Blk &B, const double *Amat, int ao,
-                                          int ak, Epi &epi) {
-  constexpr int MT = (KS + 1) / 2;
+// Generic form.  Output rows o < mo; main K rows k < mk read X[k*so + p*sp + q*sq] (stride
+// and extents from B, contracted direction DIR); optional extra K rows k = mk + r (r < next)
+// read Ext[r*esr + p*esp + q*esq] (used to fold the rank-2 face couplings of the apply into the
+// same GEMM).  A[o][k] = Amat[o*ao + k*ak] for o < mo, k < mk + next, zero beyond.
+struct LineSpec {
+  int mo, mk;                 // output rows, main K extent
+  const double *Amat; int ao, ak;
+  const double *Ext; int next, esr, esp, esq;
+};
+
+template <int DIR, int KS, int MT, class Epi>
+__device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const LineSpec &ls,
+                                            Epi &epi) {
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
-  const int md = B.m[DIR], mp = B.m[PD], mq = B.m[QD];
+  const int mo = ls.mo, mk = ls.mk, kt = ls.mk + ls.next;
+  const int mp = B.m[PD], mq = B.m[QD];
   const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -224,11 +234,16 @@ __device__ __forceinline__ void mma_lines(const double *X, const Blk &B, const d
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int o = mt * 8 + g, k = ks * 4 + t;
-      a[mt][ks] = (o < md && k < md) ? Amat[o * ao + k * ak] : 0.0;
+      a[mt][ks] = (o < mo && k < kt) ? ls.Amat[o * ls.ao + k * ls.ak] : 0.0;
     }
   int koff[KS];
+  bool kext[KS];
 #pragma unroll
-  for (int ks = 0; ks < KS; ++ks) koff[ks] = min(ks * 4 + t, md - 1) * so;
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = min(ks * 4 + t, kt - 1);
+    kext[ks] = k >= mk;
+    koff[ks] = kext[ks] ? (k - mk) * ls.esr : k * so;
+  }
   const int ptiles = (mp + 7) >> 3;
   const int ntiles = ptiles * mq;
   for (int tile = 2 * warp; tile < ntiles; tile += 2 * nw) {
@@ -242,9 +257,11 @@ __device__ __forceinline__ void mma_lines(const double *X, const Blk &B, const d
       const int tt = valid[u] ? tl : tile;
       q[u] = tt / ptiles;
       p0[u] = (tt - q[u] * ptiles) * 8;
-      const int base = min(p0[u] + g, mp - 1) * sp + q[u] * sq;
+      const int pl = min(p0[u] + g, mp - 1);
+      const double *xb = X + pl * sp + q[u] * sq;
+      const double *eb = ls.Ext ? ls.Ext + pl * ls.esp + q[u] * ls.esq : X;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) b[u][ks] = X[base + koff[ks]];
+      for (int ks = 0; ks < KS; ++ks) b[u][ks] = (kext[ks] ? eb : xb)[koff[ks]];
     }
     double c[2][MT][2];
 #pragma unroll
@@ -269,26 +286,32 @@ __device__ __forceinline__ void mma_lines(const double *X, const Blk &B, const d
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int o = mt * 8 + g;
-          if (o < md) epi.template put<DIR>(o, p, q[u], cf, c[u][mt][j]);
+          if (o < mo) epi.template put<DIR>(o, p, q[u], cf, c[u][mt][j]);
         }
       }
     }
   }
 }
 
+// Supported (KS, MT) tiles; any request is served by the smallest supported tile that covers
+// it (A is zero padded, so a larger tile is correct, only wasteful).
 template <int DIR, class Epi>
-__device__ void mma_lines_dispatch(const double *X, const Blk &B, const double *Amat, int ao,
-                                   int ak, Epi &epi) {
-  switch ((B.m[DIR] + 3) >> 2) {
-    case 1: mma_lines<DIR, 1>(X, B, Amat, ao, ak, epi); break;
-    case 2: mma_lines<DIR, 2>(X, B, Amat, ao, ak, epi); break;
-    case 3: mma_lines<DIR, 3>(X, B, Amat, ao, ak, epi); break;
-    case 4: mma_lines<DIR, 4>(X, B, Amat, ao, ak, epi); break;
-    case 5: mma_lines<DIR, 5>(X, B, Amat, ao, ak, epi); break;
-    case 6: mma_lines<DIR, 6>(X, B, Amat, ao, ak, epi); break;
-    case 7: mma_lines<DIR, 7>(X, B, Amat, ao, ak, epi); break;
-    default: mma_lines<DIR, 8>(X, B, Amat, ao, ak, epi); break;
-  }
+__device__ void mma_lines_gen(const double *X, const Blk &B, const LineSpec &ls, Epi &epi) {
+  const int KS = (ls.mk + ls.next + 3) >> 2, MT = (ls.mo + 7) >> 3;
+#define PMG_TILE(ks, mt) \
+  if (KS <= ks && MT <= mt) { mma_lines_t<DIR, ks, mt>(X, B, ls, epi); return; }
+  PMG_TILE(1, 1) PMG_TILE(2, 1) PMG_TILE(2, 2) PMG_TILE(3, 1) PMG_TILE(3, 2) PMG_TILE(3, 3)
+  PMG_TILE(4, 2) PMG_TILE(5, 2) PMG_TILE(5, 3) PMG_TILE(6, 3) PMG_TILE(7, 4) PMG_TILE(8, 4)
+#undef PMG_TILE
+  __trap();   // callers only use tiles up to K = 32, M = 32 (checked on the host)
+}
+
+// square contraction (FDM passes): A[o][k] = Amat[o*ao + k*ak], mo = mk = extent along DIR
+template <int DIR, class Epi>
+__device__ __forceinline__ void mma_lines_dispatch(const double *X, const Blk &B, const double *Amat,
+                                                   int ao, int ak, Epi &epi) {
+  const LineSpec ls = {B.m[DIR], B.m[DIR], Amat, ao, ak, nullptr, 0, 0, 0, 0};
+  mma_lines_gen<DIR>(X, B, ls, epi);
 }
 
 template <int DIR>
@@ -322,6 +345,16 @@ struct EpiWeightStore {
   }
   template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
     Zg[blk_index<DIR>(G, o, p, q)] = v * (cf * W[DIR][o]);
+  }
+};
+// plain accumulation into V (first pass stores)
+struct EpiAcc {
+  double *V; Blk B; bool first;
+  template <int DIR> __device__ __forceinline__ double col(int, int) const { return 0.0; }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double, double v) const {
+    const int w = blk_index<DIR>(B, o, p, q);
+    if (first) V[w] = v;
+    else V[w] += v;
   }
 };
 // mass-weighted accumulation of one term of Eq. 7 into V
@@ -408,70 +441,72 @@ __global__ void __launch_bounds__(256, 2) k_fdm_mma(LevelDev L, const double *__
   mma_lines_dispatch<0>(X, B, Ss[0], m[0], 1, ws);
 }
 
-// smem: U (n^3) | V (n^3) | D_x, D_y, D_z (n^2) | traces 3 x 4n | mass 3 x n
-__global__ void __launch_bounds__(256) k_apply_mma(LevelDev L, const double *__restrict__ u,
-                                                   const double *__restrict__ T,
-                                                   const double *__restrict__ f,
-                                                   double *__restrict__ out) {
+// smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
+// Per direction d the line GEMM is  V += M_p M_q [D | a ap b bp] [U-lines ; c1 c2 c3 c4]  where
+// c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
+// c1 = -tdR/2 - mu tvR, c2 = tvR/2, c3 = tdL/2 - mu tvL, c4 = -tvL/2.
+__global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+                                                      const double *__restrict__ T,
+                                                      const double *__restrict__ f,
+                                                      double *__restrict__ out) {
   extern __shared__ double sm[];
   const int n = L.n, n2 = n * n, n3 = n2 * n;
-  double *U = sm, *V = sm + n3, *Ds = sm + 2 * n3;
-  double *trs = Ds + 3 * n2, *ms = trs + 12 * n;
+  double *U = sm, *V = sm + n3, *Cf = sm + 2 * n3, *ms = Cf + 12 * n2;
   const int e = blockIdx.x;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  const int ecoord[3] = {ex, ey, ez};
+  const int edim[3] = {L.nx, L.ny, L.nz};
   stage(U, u + (long long)e * n3, n3);
   for (int d = 0; d < 3; ++d) {
-    stage(Ds + d * n2, L.D[d], n2);
-    stage(trs + d * 4 * n, L.tr[d], 4 * n);
+    int c[3] = {ex, ey, ez};
+    c[d] = wrap(ecoord[d] + 1, edim[d]);
+    stage(Cf + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
+          2 * n2);                                                   // tvR, tdR of the right nb
+    c[d] = wrap(ecoord[d] - 1, edim[d]);
+    stage(Cf + d * 4 * n2 + 2 * n2,
+          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
     stage(ms + d * n, L.mass[d], n);
   }
   cp_async_wait_all();
   __syncthreads();
-  const double *mass[3] = {ms, ms + n, ms + 2 * n};
-  const Blk B = {{n, n, n}, {1, n, n2}};
-  EpiMassAcc acc{V, B, {mass[0], mass[1], mass[2]}, true};
-  mma_lines_dispatch<0>(U, B, Ds, n, 1, acc); __syncthreads();
-  acc.first = false;
-  mma_lines_dispatch<1>(U, B, Ds + n2, n, 1, acc); __syncthreads();
-  mma_lines_dispatch<2>(U, B, Ds + 2 * n2, n, 1, acc); __syncthreads();
-  // rank-2 neighbour couplings (E+ u_{e+1}, E- u_{e-1}) from the neighbours' face traces,
-  // staged into the (now free) U buffer, or behind the tables when 12 n^2 > n^3:
-  // per direction [tvR | tdR | tvL | tdL] x n^2
-  double *TS = (12 * n2 > n3) ? ms + 3 * n : U;
-  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
-  const int ecoord[3] = {ex, ey, ez};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  for (int d = 0; d < 3; ++d) {
-    int c[3] = {ex, ey, ez};
-    c[d] = wrap(ecoord[d] + 1, edim[d]);
-    stage(TS + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
-          2 * n2);
-    c[d] = wrap(ecoord[d] - 1, edim[d]);
-    stage(TS + d * 4 * n2 + 2 * n2,
-          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, pp = t - d * n2;
+    double *C = Cf + d * 4 * n2 + pp;
+    const double mu = L.mu[d];
+    const double tvR = C[0], tdR = C[n2], tvL = C[2 * n2], tdL = C[3 * n2];
+    C[0] = -0.5 * tdR - mu * tvR;
+    C[n2] = 0.5 * tvR;
+    C[2 * n2] = 0.5 * tdL - mu * tvL;
+    C[3 * n2] = -0.5 * tvL;
   }
-  cp_async_wait_all();
   __syncthreads();
-  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
-    const int i = t % n, j = (t / n) % n, k = t / n2;
-    const int idx[3] = {i, j, k};
-    const int pf[3] = {j + n * k, i + n * k, i + n * j};
-    double v = V[t];
-    double s3[3];
+  const Blk B = {{n, n, n}, {1, n, n2}};
+  EpiAcc acc{V, B, true};
+  LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
+  mma_lines_gen<0>(U, B, lx, acc); __syncthreads();
+  acc.first = false;
+  LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
+  mma_lines_gen<1>(U, B, ly, acc); __syncthreads();
+  LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
+  mma_lines_gen<2>(U, B, lz, acc); __syncthreads();
+  // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism
+  const long long g0 = (long long)e * n3;
+  constexpr int UNR = 4;
+  for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
+    double fv[UNR];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double *tr = trs + d * 4 * n;
-      const int id = idx[d];
-      const double *Tn = TS + d * 4 * n2;
-      const double tvR = Tn[pf[d]], tdR = Tn[n2 + pf[d]];
-      const double tvL = Tn[2 * n2 + pf[d]], tdL = Tn[3 * n2 + pf[d]];
-      const double mu = L.mu[d];
-      s3[d] = tr[id] * (-0.5 * tdR - mu * tvR) + tr[n + id] * (0.5 * tvR)
-            + tr[2 * n + id] * (0.5 * tdL - mu * tvL) + tr[3 * n + id] * (-0.5 * tvL);
+    for (int q = 0; q < UNR; ++q) {
+      const int t = t0 + q * blockDim.x;
+      fv[q] = (f && t < n3) ? __ldg(f + g0 + t) : 0.0;
     }
-    v += mass[2][k] * mass[1][j] * s3[0] + mass[2][k] * mass[0][i] * s3[1]
-       + mass[1][j] * mass[0][i] * s3[2];
-    const long long gi = (long long)e * n3 + t;
-    out[gi] = f ? __ldg(f + gi) - v : v;
+#pragma unroll
+    for (int q = 0; q < UNR; ++q) {
+      const int t = t0 + q * blockDim.x;
+      if (t >= n3) break;
+      const int i = t % n, j = (t / n) % n, k = t / n2;
+      const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
+      out[g0 + t] = f ? fv[q] - v : v;
+    }
   }
 }
 
@@ -544,6 +579,149 @@ __global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restr
     }
     const long long g = (long long)e * n3 + t;
     u[g] = zero ? du : u[g] + du;
+  }
+}
+
+// Shared-memory fold (Eq. 10 scatter, deterministic): the element's DOFs are staged in shared
+// memory, the weighted corrections of the 27 subdomains whose windows touch this element are
+// added sub-box by sub-box in a fixed order (own subdomain first, then the 26 neighbours),
+// u is written back coalesced and, optionally, the face traces of the updated u are emitted
+// (fusing the trace kernel of the following residual).
+__device__ __forceinline__ int src_off(int code) { return code == 0 ? 0 : (code == 1 ? -1 : 1); }
+
+__global__ void __launch_bounds__(256) k_fold_sm(LevelDev L, const double *__restrict__ Z,
+                                                 double *__restrict__ u, int zero,
+                                                 double *__restrict__ T) {
+  extern __shared__ double sm[];
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int mx = L.m[0], my = L.m[1], Mw = L.Mw;
+  double *U = sm, *trs = sm + n3;
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  if (zero) {
+    for (int t = threadIdx.x; t < n3; t += blockDim.x) U[t] = 0.0;
+  } else {
+    stage(U, u + (long long)e * n3, n3);
+  }
+  if (T)
+    for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int src = 0; src < 27; ++src) {
+    const int oc[3] = {src % 3, (src / 3) % 3, src / 9};
+    int lo[3], cnt[3], woff[3], sc[3];
+    bool empty = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int no = L.no[d], o = src_off(oc[d]);
+      if (o == 0) { lo[d] = 0; cnt[d] = n; woff[d] = no; }
+      else if (o == -1) { lo[d] = 0; cnt[d] = no; woff[d] = no + n; }   // e is the right nb of s
+      else { lo[d] = n - no; cnt[d] = no; woff[d] = no - n; }           // e is the left nb of s
+      empty |= cnt[d] == 0;
+      sc[d] = wrap(ec[d] + o, edim[d]);
+    }
+    if (empty) continue;
+    const double *Zs = Z + (long long)(sc[0] + L.nx * (sc[1] + L.ny * sc[2])) * Mw;
+    const int total = cnt[0] * cnt[1] * cnt[2];
+    constexpr int UNR = 4;
+    for (int w0 = threadIdx.x; w0 < total; w0 += UNR * blockDim.x) {
+      double zv[UNR];
+      int li[UNR];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int w = w0 + q * blockDim.x;
+        li[q] = -1;
+        zv[q] = 0.0;
+        if (w < total) {
+          const int a = w % cnt[0], r = w / cnt[0];
+          const int b = r % cnt[1], c = r / cnt[1];
+          const int i = lo[0] + a, j = lo[1] + b, k = lo[2] + c;
+          li[q] = i + n * (j + n * k);
+          zv[q] = __ldg(Zs + (woff[0] + i) + mx * ((woff[1] + j) + my * (woff[2] + k)));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q)
+        if (li[q] >= 0) U[li[q]] += zv[q];
+    }
+    __syncthreads();
+  }
+  double *ue = u + (long long)e * n3;
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
+  if (!T) return;
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = U[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
+// Register-only fold: one thread per DOF issues all (up to 27) predicated loads of the
+// weighted window values that cover it before summing them in a fixed order -> maximal
+// memory-level parallelism, deterministic result.  NT = compile-time n (fast index math).
+template <int NT>
+__global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restrict__ Z,
+                                               double *__restrict__ u, int zero) {
+  const int n = NT > 0 ? NT : L.n;
+  const int n3 = n * n * n;
+  const int mx = L.m[0], my = L.m[1];
+  const long long Mw = L.Mw;
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  int se[3][3];                       // source subdomain coordinate per direction: o = -1, 0, +1
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
+  const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int i = t % n, j = (t / n) % n, k = t / (n * n);
+    const int idx[3] = {i, j, k};
+    const int nod[3] = {no0, no1, no2};
+    bool v[3][3];
+    int wi[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int no = nod[d], id = idx[d];
+      v[d][0] = id < no;        wi[d][0] = no + n + id;     // left-neighbour subdomain
+      v[d][1] = true;           wi[d][1] = no + id;         // own subdomain
+      v[d][2] = id >= n - no;   wi[d][2] = id - (n - no);   // right-neighbour subdomain
+    }
+    const long long g = (long long)e * n3 + t;
+    double du = zero ? 0.0 : u[g];
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      if (!v[2][oz]) continue;
+      double z[9];
+#pragma unroll
+      for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          const bool ok = v[0][ox] && v[1][oy];
+          const long long sidx = se[0][ox] + L.nx * (se[1][oy] + (long long)L.ny * se[2][oz]);
+          z[ox + 3 * oy] = ok ? __ldg(Z + sidx * Mw + wi[0][ox] + mx * (wi[1][oy] + my * wi[2][oz])) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) du += z[q];
+    }
+    u[g] = du;
   }
 }
 
@@ -781,7 +959,7 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
   const int n = L.n;
   if (n <= 20) {
     const size_t n2 = (size_t)n * n, n3 = n2 * n;
-    const size_t sb = sizeof(double) * (2 * n3 + 3 * n2 + 15 * n + (12 * n2 > n3 ? 12 * n2 : 0));
+    const size_t sb = sizeof(double) * (2 * n3 + 12 * n2 + 3 * n);
     static size_t configured = 0;
     if (sb > 48 * 1024 && sb > configured) {
       cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
@@ -827,9 +1005,20 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
   }
   return cudaGetLastError();
 }
-cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, cudaStream_t s) {
-  k_fold<<<L.Ne, 256, 0, s>>>(L, Z, u, zero ? 1 : 0);
-  return cudaGetLastError();
+cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
+                        cudaStream_t s) {
+  const int z = zero ? 1 : 0;
+  switch (L.n) {
+    case 3: k_fold2<3><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+    case 5: k_fold2<5><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+    case 9: k_fold2<9><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+    case 17: k_fold2<17><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+    case 33: k_fold2<33><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+    default: k_fold2<0><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && T) e = launch_traces(L, u, T, s);
+  return e;
 }
 static size_t xfer_smem(int nf, int nc) {
   return sizeof(double) * ((size_t)nc * nf * nf + (size_t)nc * nc * nf);

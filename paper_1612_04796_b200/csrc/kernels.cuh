@@ -17,6 +17,7 @@ struct LevelDev {
   const double *lam[3];    // m
   const double *W[3];      // m
   const double *nodes;     // n reference nodes
+  const double *Daug[3];   // [D | a ap b bp], n x (n+4) row-major (apply line GEMM)
   int Mw;                  // m0*m1*m2
 };
 
@@ -32,7 +33,9 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
                          double *out, cudaStream_t s);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
-cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, cudaStream_t s);
+// fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
+cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
+                        cudaStream_t s);
 cudaError_t launch_restrict(const LevelDev &Lf, int nc, const double *I, const double *rf,
                             double *fc, cudaStream_t s);
 cudaError_t launch_prolong(const LevelDev &Lf, int nc, const double *I, const double *uc,
