@@ -280,10 +280,18 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
     const int nu = c->nu1[l];
     if ((st = smooth_impl(c, l, U[l], F[l], nu, zero, s, true))) return st;   // l.290
     double *r = wsp<double>(c, c->lev[l].o_r);
-    if ((st = residual_impl(c, l, U[l], F[l], r, s, nu > 0))) return st;      // l.292
     pmg::LevelDev d = level_dev(c, l);
-    LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n, wsp<double>(c, c->lev[l].o_interp), r,
-                                   F[l - 1], s));
+    if (pmg::apply_pipe_ok(d)) {                                     // l.292 fused
+      double *T = wsp<double>(c, c->lev[l].o_T);
+      if (nu == 0) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, U[l], T, s));
+      LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply_pipe(d, U[l], T, F[l], nullptr,
+                                                       wsp<double>(c, c->lev[l].o_interp),
+                                                       c->lev[l - 1].n, F[l - 1], s));
+    } else {
+      if ((st = residual_impl(c, l, U[l], F[l], r, s, nu > 0))) return st;    // l.292
+      LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n,
+                                     wsp<double>(c, c->lev[l].o_interp), r, F[l - 1], s));
+    }
   }
   if ((st = coarse_impl(c, F[0], U[0], s))) return st;           // l.295
   for (int l = 1; l <= L; ++l) {                                  // l.298

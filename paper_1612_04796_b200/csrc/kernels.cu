@@ -5,6 +5,8 @@
 // Face-trace buffer T (per level): T[((e*3 + d)*4 + q)*n^2 + p], q = 0 left value,
 // 1 left (2/D)-derivative, 2 right value, 3 right derivative; p = in-face node index
 // (x-faces: j + n k, y-faces: i + n k, z-faces: i + n j).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace pmg {
@@ -225,6 +227,8 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
   const int mo = ls.mo, mk = ls.mk, kt = ls.mk + ls.next;
   const int mp = B.m[PD], mq = B.m[QD];
+  const int ncol = mp * mq;                                 // columns (p, q), p fastest
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)mp + 1u;   // q = umulhi(n, magic) = n / mp
   const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -244,22 +248,15 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
     kext[ks] = k >= mk;
     koff[ks] = kext[ks] ? (k - mk) * ls.esr : k * so;
   }
-  const int ptiles = (mp + 7) >> 3;
-  const int ntiles = ptiles * mq;
+  const int ntiles = (ncol + 7) >> 3;
   for (int tile = 2 * warp; tile < ntiles; tile += 2 * nw) {
-    int p0[2], q[2];
-    bool valid[2];
     double b[2][KS];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int tl = tile + u;
-      valid[u] = tl < ntiles;
-      const int tt = valid[u] ? tl : tile;
-      q[u] = tt / ptiles;
-      p0[u] = (tt - q[u] * ptiles) * 8;
-      const int pl = min(p0[u] + g, mp - 1);
-      const double *xb = X + pl * sp + q[u] * sq;
-      const double *eb = ls.Ext ? ls.Ext + pl * ls.esp + q[u] * ls.esq : X;
+      const int nb = min(min(tile + u, ntiles - 1) * 8 + g, ncol - 1);
+      const int q = __umulhi((unsigned)nb, magic), p = nb - q * mp;
+      const double *xb = X + p * sp + q * sq;
+      const double *eb = ls.Ext ? ls.Ext + p * ls.esp + q * ls.esq : X;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) b[u][ks] = (kext[ks] ? eb : xb)[koff[ks]];
     }
@@ -277,16 +274,17 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      if (!valid[u]) continue;
+      if (tile + u >= ntiles) continue;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int p = p0[u] + 2 * t + j;
-        if (p >= mp) continue;
-        const double cf = epi.template col<DIR>(p, q[u]);
+        const int n = (tile + u) * 8 + 2 * t + j;
+        if (n >= ncol) continue;
+        const int q = __umulhi((unsigned)n, magic), p = n - q * mp;
+        const double cf = epi.template col<DIR>(p, q);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int o = mt * 8 + g;
-          if (o < mo) epi.template put<DIR>(o, p, q[u], cf, c[u][mt][j]);
+          if (o < mo) epi.template put<DIR>(o, p, q, cf, c[u][mt][j]);
         }
       }
     }
@@ -448,7 +446,9 @@ __global__ void __launch_bounds__(256, 2) k_fdm_mma(LevelDev L, const double *__
 __global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
                                                       const double *__restrict__ T,
                                                       const double *__restrict__ f,
-                                                      double *__restrict__ out) {
+                                                      double *__restrict__ out,
+                                                      const double *__restrict__ restrict_I,
+                                                      int nc, double *__restrict__ fc) {
   extern __shared__ double sm[];
   const int n = L.n, n2 = n * n, n3 = n2 * n;
   double *U = sm, *V = sm + n3, *Cf = sm + 2 * n3, *ms = Cf + 12 * n2;
@@ -505,9 +505,141 @@ __global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *
       if (t >= n3) break;
       const int i = t % n, j = (t / n) % n, k = t / n2;
       const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
-      out[g0 + t] = f ? fv[q] - v : v;
+      const double rr = f ? fv[q] - v : v;
+      if (restrict_I) V[t] = rr;
+      else out[g0 + t] = rr;
     }
   }
+  if (restrict_I) {
+    // fused residual restriction f_c = (I^T (x) I^T (x) I^T) r (Alg. 1 l.292): r stays in V;
+    // x pass (n -> nc) into U, y pass into Cf, z pass straight to the coarse vector
+    __syncthreads();
+    const Blk T1 = {{nc, n, n}, {1, nc, nc * n}};
+    const Blk T2 = {{nc, nc, n}, {1, nc, nc * nc}};
+    const Blk FC = {{nc, nc, nc}, {1, nc, nc * nc}};
+    const LineSpec rx = {nc, n, restrict_I, 1, nc, nullptr, 0, 0, 0, 0};
+    EpiStore s1{U, T1};
+    mma_lines_gen<0>(V, B, rx, s1); __syncthreads();
+    EpiStore s2{Cf, T2};
+    mma_lines_gen<1>(U, T1, rx, s2); __syncthreads();
+    EpiStore s3{fc + (long long)e * nc * nc * nc, FC};
+    mma_lines_gen<2>(Cf, T2, rx, s3);
+  }
+}
+
+// Persistent, double-buffered operator apply / residual (+ optional fused restriction).
+// One CTA per SM walks elements e = blockIdx.x, +gridDim.x, ...; while element e is computed
+// from buffer b, the cp.async loads of the next element (u block and neighbour face traces)
+// stream into buffer b^1, so HBM stays busy.  Per element: V = sum_d line-GEMM_d (augmented
+// K, see k_apply_mma), then r = f - M V (or M V) to global, or -- with `restrict_I` -- r stays in
+// shared memory and f_c = I^T r is computed by three more line GEMMs and written to the
+// coarse level (Alg. 1 l.292 fused: no global r).
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void apply_issue_loads(const LevelDev &L, int e, const double *u,
+                                                  const double *T, double *U, double *Cf) {
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  const int ecoord[3] = {ex, ey, ez};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  stage(U, u + (long long)e * n3, n3);
+  for (int d = 0; d < 3; ++d) {
+    int c[3] = {ex, ey, ez};
+    c[d] = wrap(ecoord[d] + 1, edim[d]);
+    stage(Cf + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
+          2 * n2);
+    c[d] = wrap(ecoord[d] - 1, edim[d]);
+    stage(Cf + d * 4 * n2 + 2 * n2,
+          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
+  }
+}
+
+// smem: U[2] (n^3 each) | Cf[2] (12 n^2 each) | V (n^3) | mass (3n)
+__global__ void __launch_bounds__(512, 1) k_apply_pipe(LevelDev L, const double *__restrict__ u,
+                                                       const double *__restrict__ T,
+                                                       const double *__restrict__ f,
+                                                       double *__restrict__ out,
+                                                       const double *__restrict__ restrict_I,
+                                                       int nc, double *__restrict__ fc) {
+  extern __shared__ double sm[];
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  double *Ub[2] = {sm, sm + n3};
+  double *Cb[2] = {sm + 2 * n3, sm + 2 * n3 + 12 * n2};
+  double *V = sm + 2 * n3 + 24 * n2;
+  double *ms = V + n3;
+  for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
+  int e = blockIdx.x;
+  if (e < L.Ne) apply_issue_loads(L, e, u, T, Ub[0], Cb[0]);
+  cp_async_commit();
+  int b = 0;
+  const Blk B = {{n, n, n}, {1, n, n2}};
+  for (; e < L.Ne; e += gridDim.x) {
+    const int en = e + gridDim.x;
+    if (en < L.Ne) apply_issue_loads(L, en, u, T, Ub[b ^ 1], Cb[b ^ 1]);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double *U = Ub[b], *Cf = Cb[b];
+    for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+      const int d = t / n2, pp = t - d * n2;
+      double *C = Cf + d * 4 * n2 + pp;
+      const double mu = L.mu[d];
+      const double tvR = C[0], tdR = C[n2], tvL = C[2 * n2], tdL = C[3 * n2];
+      C[0] = -0.5 * tdR - mu * tvR;
+      C[n2] = 0.5 * tvR;
+      C[2 * n2] = 0.5 * tdL - mu * tvL;
+      C[3 * n2] = -0.5 * tvL;
+    }
+    __syncthreads();
+    EpiAcc acc{V, B, true};
+    LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
+    mma_lines_gen<0>(U, B, lx, acc); __syncthreads();
+    acc.first = false;
+    LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
+    mma_lines_gen<1>(U, B, ly, acc); __syncthreads();
+    LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
+    mma_lines_gen<2>(U, B, lz, acc); __syncthreads();
+    const long long g0 = (long long)e * n3;
+    constexpr int UNR = 4;
+    for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
+      double fv[UNR];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int t = t0 + q * blockDim.x;
+        fv[q] = (f && t < n3) ? __ldg(f + g0 + t) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int t = t0 + q * blockDim.x;
+        if (t >= n3) break;
+        const int i = t % n, j = (t / n) % n, k = t / n2;
+        const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
+        const double rr = f ? fv[q] - v : v;
+        if (restrict_I) V[t] = rr;
+        else out[g0 + t] = rr;
+      }
+    }
+    if (restrict_I) {
+      __syncthreads();
+      // f_c = (I^T (x) I^T (x) I^T) r: x (n -> nc) into U, y into Cf, z to global
+      const Blk R = B;
+      const Blk T1 = {{nc, n, n}, {1, nc, nc * n}};
+      const Blk T2 = {{nc, nc, n}, {1, nc, nc * nc}};
+      const Blk FC = {{nc, nc, nc}, {1, nc, nc * nc}};
+      EpiStore s1{U, T1};
+      LineSpec rx = {nc, n, restrict_I, 1, nc, nullptr, 0, 0, 0, 0};
+      mma_lines_gen<0>(V, R, rx, s1); __syncthreads();
+      EpiStore s2{Cf, T2};
+      mma_lines_gen<1>(U, T1, rx, s2); __syncthreads();
+      EpiStore s3{fc + (long long)e * nc * nc * nc, FC};
+      mma_lines_gen<2>(Cf, T2, rx, s3);
+    }
+    __syncthreads();
+    b ^= 1;
+  }
+  cp_async_wait<0>();
 }
 
 // Face traces with the element staged in shared memory (coalesced loads).
@@ -954,9 +1086,45 @@ cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStr
   }
   return cudaGetLastError();
 }
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static size_t apply_pipe_smem(int n) {
+  const size_t n2 = (size_t)n * n, n3 = n2 * n;
+  return sizeof(double) * (3 * n3 + 24 * n2 + 3 * n);
+}
+
+bool apply_pipe_ok(const LevelDev &L) { return L.n <= 17; }
+
+static size_t apply_mma_smem(int n) {
+  const size_t n2 = (size_t)n * n, n3 = n2 * n;
+  return sizeof(double) * (2 * n3 + 12 * n2 + 3 * n);
+}
+
+cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
+                              double *out, const double *I, int nc, double *fc, cudaStream_t s) {
+  const size_t sb = apply_mma_smem(L.n);
+  static size_t configured = 0;
+  if (sb > 48 * 1024 && sb > configured) {
+    cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    configured = sb;
+  }
+  k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
                          double *out, cudaStream_t s) {
   const int n = L.n;
+
   if (n <= 20) {
     const size_t n2 = (size_t)n * n, n3 = n2 * n;
     const size_t sb = sizeof(double) * (2 * n3 + 12 * n2 + 3 * n);
@@ -965,7 +1133,7 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
       cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
       configured = sb;
     }
-    k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out);
+    k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out, nullptr, 0, nullptr);
   } else {
     k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
   }

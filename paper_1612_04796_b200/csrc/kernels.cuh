@@ -31,6 +31,10 @@ struct CoarseDev {
 cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s);
 cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
                          double *out, cudaStream_t s);
+// fused residual + restriction f_c = I^T (f - A u) (no global r); available when apply_pipe_ok
+bool apply_pipe_ok(const LevelDev &L);
+cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
+                              double *out, const double *I, int nc, double *fc, cudaStream_t s);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
