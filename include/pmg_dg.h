@@ -104,6 +104,11 @@ int dg_coarse_solve(dg_ctx *ctx, const double *f0, double *u0, void *stream);
  * unused).  Default: 1, 1 on all levels (fixed V(1,1)). Host-only. */
 int dg_set_schedule(dg_ctx *ctx, const int *nu1, const int *nu2);
 
+/* Replay V-cycles (pmg_vcycle and the preconditioner inside pcg_solve) from cached CUDA graphs
+ * (default on).  A graph is captured on first use per (u, f) pointer pair and replayed on the
+ * caller's stream; while profiling (dg_profile) launches are issued eagerly instead. */
+int dg_set_graphs(dg_ctx *ctx, int enable);
+
 /* pmg_vcycle — one multigrid V-cycle, Algorithm 1, in place on u
  * (top level), with the schedule above.  f is read-only. */
 int pmg_vcycle(dg_ctx *ctx, double *u, const double *f, void *stream);

@@ -40,6 +40,7 @@ _sig = {
     "dg_rhs_sin": (_i, [_vp, _d, _d, _d, _d, _vp, _vp]),
     "dg_launch_count": (_ll, [_vp]),
     "dg_profile": (_i, [_vp, _i]),
+    "dg_set_graphs": (_i, [_vp, _i]),
     "dg_profile_read": (_i, [_vp, _dp, C.POINTER(_ll), _i]),
     "pmg_fp64_peak": (_i, [_i, _dp, _vp]),
     "dg_last_error": (C.c_char_p, [_vp]),
@@ -117,6 +118,9 @@ class DG:
         return lib.dg_launch_count(self._c)
 
     PROF_KINDS = ("traces", "apply", "fdm", "fold", "restrict", "prolong", "coarse", "vec")
+
+    def set_graphs(self, enable=True):
+        self._check(lib.dg_set_graphs(self._c, 1 if enable else 0))
 
     def profile(self, enable=True):
         self._check(lib.dg_profile(self._c, 1 if enable else 0))

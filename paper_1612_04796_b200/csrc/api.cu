@@ -59,7 +59,13 @@ struct dg_ctx {
   std::vector<int> nu1, nu2;
   double *host_pinned = nullptr;
   long long launches = 0;
+  long long launches_per_cycle = 0;
   std::string err;
+  // CUDA-graph replay of whole V-cycles (dg_set_graphs); keyed by (u, f, zero_top)
+  bool graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry { double *u; const double *f; bool zero; cudaGraphExec_t exec; };
+  std::vector<GraphEntry> graph_cache;
   // optional per-kernel CUDA-event timing (dg_profile): slot = kind * 8 + level
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -250,6 +256,11 @@ int coarse_impl(dg_ctx *c, const double *f0, double *u0, cudaStream_t s) {
   double *part = wsp<double>(c, c->o_part);
   double *scal = wsp<double>(c, c->o_scal);
   double *G1 = wsp<double>(c, c->o_G1), *G2 = wsp<double>(c, c->o_G2);
+  if (c->G[2] <= 32) {
+    LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_fused(d0, C, f0, G1, G2, u0, s));
+    c->launches += 4;   // launch_coarse_fused issues 5 kernels
+    return PMG_OK;
+  }
   LAUNCHK(c, K_COARSE, 0, s, pmg::launch_sum(f0, N0, part, scal + 10, 1.0 / N0, s));           // mean(f0)
   LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_gather(d0, C, f0, scal + 10, G1, s));          // project
   LAUNCHK(c, K_COARSE, 0, s, pmg::launch_lex_contract(C, 0, true, G1, G2, s));
@@ -301,6 +312,38 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
     if ((st = smooth_impl(c, l, U[l], F[l], c->nu2[l], false, s))) return st;  // l.301
   }
   return PMG_OK;
+}
+
+// V-cycle through a cached CUDA graph: the ~5 launches per level become one graph launch
+// (launch latency dominates the small configurations).  Captured on an internal stream, then
+// replayed on the caller's stream.  Falls back to eager launches while profiling.
+int vcycle_run(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream_t s) {
+  if (!c->graphs || c->prof) return vcycle_impl(c, u, f, zero_top, s);
+  for (auto &g : c->graph_cache)
+    if (g.u == u && g.f == f && g.zero == zero_top) {
+      c->launches += c->launches_per_cycle;
+      return cuda_check(c, cudaGraphLaunch(g.exec, s), "cudaGraphLaunch");
+    }
+  cudaError_t e = cudaSuccess;
+  if (!c->cap_stream) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaStreamCreate");
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaStreamBeginCapture");
+  const long long l0 = c->launches;
+  int st = vcycle_impl(c, u, f, zero_top, c->cap_stream);
+  e = cudaStreamEndCapture(c->cap_stream, &graph);
+  if (st) { if (graph) cudaGraphDestroy(graph); return st; }
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaStreamEndCapture");
+  c->launches_per_cycle = c->launches - l0;
+  c->launches = l0;
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaGraphInstantiate");
+  c->graph_cache.push_back({u, f, zero_top, exec});
+  c->launches += c->launches_per_cycle;
+  return cuda_check(c, cudaGraphLaunch(exec, s), "cudaGraphLaunch");
 }
 
 }  // namespace
@@ -563,6 +606,8 @@ int dg_set_schedule(dg_ctx *c, const int *nu1, const int *nu2) {
   for (int l = 1; l <= c->L; ++l)
     if (nu1[l] < 0 || nu2[l] < 0) return fail(c, PMG_EINVAL, "negative smoothing count");
   for (int l = 0; l <= c->L; ++l) { c->nu1[l] = nu1[l]; c->nu2[l] = nu2[l]; }
+  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
+  c->graph_cache.clear();
   return PMG_OK;
 }
 
@@ -571,7 +616,7 @@ int pmg_vcycle(dg_ctx *c, double *u, const double *f, void *stream) {
   if (st) return st;
   if (!c->schwarz_ready) return fail(c, PMG_ESTATE, "dg_schwarz_setup not called");
   if (!u || !f || u == f) return fail(c, PMG_EINVAL, "pmg_vcycle: bad arguments");
-  return vcycle_impl(c, u, f, false, S(stream));
+  return vcycle_run(c, u, f, false, S(stream));
 }
 
 int pcg_solve(dg_ctx *c, double *u, const double *f, double rtol, int maxit, int *iters,
@@ -602,7 +647,7 @@ int pcg_solve(dg_ctx *c, double *u, const double *f, double rtol, int maxit, int
   if (iters) *iters = 0;
   if (!std::isfinite(r0)) return fail(c, PMG_EDIVERGED, "non-finite initial residual");
   if (r0 == 0) return PMG_OK;
-  if ((st = vcycle_impl(c, z, r, true, s))) return st;                  // z0 = V(0, r0)
+  if ((st = vcycle_run(c, z, r, true, s))) return st;                   // z0 = V(0, r0)
   LAUNCH(c, pmg::launch_copy(p, z, N, s));                              // p0 = z0
   LAUNCH(c, pmg::launch_zr_beta(z, r, r, N, part, scal, true, s));      // zr = <z0, r0>
   for (int k = 1; k <= maxit; ++k) {
@@ -617,7 +662,7 @@ int pcg_solve(dg_ctx *c, double *u, const double *f, double rtol, int maxit, int
     if (!std::isfinite(rn) || rn > 1e3 * r0) return fail(c, PMG_EDIVERGED, "PCG diverged");
     if (rn <= rtol * r0) return PMG_OK;
     if (k == maxit) break;
-    if ((st = vcycle_impl(c, z, r, true, s))) return st;                // z = V(0, r)
+    if ((st = vcycle_run(c, z, r, true, s))) return st;                 // z = V(0, r)
     LAUNCH(c, pmg::launch_zr_beta(z, r, rold, N, part, scal, false, s));  // beta (Golub-Ye)
     LAUNCH(c, pmg::launch_p_update(p, z, N, scal, s));                  // p = z + beta p
   }
@@ -663,6 +708,12 @@ int dg_rhs_sin(dg_ctx *c, double amp, double kx, double ky, double kz, double *b
 
 long long dg_launch_count(const dg_ctx *c) { return c ? c->launches : -1; }
 
+int dg_set_graphs(dg_ctx *c, int enable) {
+  if (!c) return PMG_EINVAL;
+  c->graphs = enable != 0;
+  return PMG_OK;
+}
+
 int dg_profile(dg_ctx *c, int enable) {
   if (!c) return PMG_EINVAL;
   c->prof = enable != 0;
@@ -694,6 +745,8 @@ void dg_destroy(dg_ctx *c) {
   if (!c) return;
   if (c->host_pinned) cudaFreeHost(c->host_pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
 

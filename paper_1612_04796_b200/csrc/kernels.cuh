@@ -49,6 +49,9 @@ cudaError_t launch_coarse_gather(const LevelDev &L0, const CoarseDev &C, const d
                                  const double *mean, double *G, cudaStream_t s);
 cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, const double *in,
                                 double *out, cudaStream_t s);
+// whole coarse solve in 5 launches (needs 2 n_e <= 32 along z; see kernels.cu)
+cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                double *G1, double *G2, double *u0, cudaStream_t s);
 cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s);
 cudaError_t launch_coarse_scatter(const LevelDev &L0, const CoarseDev &C, const double *G,
                                   const double *mean, double *u0, cudaStream_t s);
