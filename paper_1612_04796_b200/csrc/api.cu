@@ -2,6 +2,7 @@
 // arXiv:1612.04796, Algorithm 1 and §3.2.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -28,7 +29,8 @@ struct LevelHost {
   std::vector<double> mass[3], D[3], tr[3], S[3], lam[3], W[3], interp, nodes, Daug[3];
   // workspace byte offsets
   size_t o_mass[3], o_D[3], o_tr[3], o_S[3], o_lam[3], o_W[3], o_Daug[3], o_interp = 0, o_nodes = 0;
-  size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0;
+  size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0, o_scr2 = 0, o_cb = 0, o_v = 0;
+  int fdm_path = 0;          // 0: DMMA in shared memory, 1: global-memory line GEMMs, 2: generic
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
   ld lam_min[3] = {0, 0, 0}, lam_max[3] = {0, 0, 0};
@@ -155,10 +157,24 @@ void plan_workspace(dg_ctx *c) {
     h.o_T = p.dbl(Ne * 12 * n * n);
     if (l >= 1 && c->schwarz_ready) {
       h.o_Z = p.dbl(Ne * h.Mw);
+      size_t mma_words = (size_t)h.Mw;
+      int mmax = 0;
+      for (int d = 0; d < 3; ++d) {
+        mma_words += (size_t)h.m[d] * h.m[d] + 3 * (size_t)h.m[d];
+        mmax = std::max(mmax, h.m[d]);
+      }
+      if (mmax <= 32 && mma_words * sizeof(double) <= FDM_SMEM_MAX) h.fdm_path = 0;
+      else if (mmax <= 48) h.fdm_path = 1;
+      else h.fdm_path = 2;
       const size_t sb = sizeof(double) * (2 * (size_t)h.Mw);
       h.fdm_smem = sb <= FDM_SMEM_MAX;
       h.fdm_smem_bytes = h.fdm_smem ? sb : 0;
-      h.o_scr = h.fdm_smem ? 0 : p.dbl(Ne * h.Mw);
+      h.o_scr = (h.fdm_path == 1 || !h.fdm_smem) ? p.dbl(Ne * h.Mw) : 0;
+      h.o_scr2 = h.fdm_path == 1 ? p.dbl(Ne * h.Mw) : 0;
+    }
+    if (n > 17) {                    // global-memory apply buffers (face coefficients, V)
+      h.o_cb = p.dbl(Ne * 12 * n * n);
+      h.o_v = p.dbl(h.N);
     }
   }
   for (int d = 0; d < 3; ++d) {
@@ -219,7 +235,13 @@ int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *ou
   pmg::LevelDev d = level_dev(c, l);
   double *T = wsp<double>(c, c->lev[l].o_T);
   if (!have_traces) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
-  LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply(d, u, T, f, out, s));
+  if (c->lev[l].o_cb) {
+    LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply_global(d, u, T, f, out, wsp<double>(c, c->lev[l].o_cb),
+                                                       wsp<double>(c, c->lev[l].o_v), s));
+    c->launches += 4;
+  } else {
+    LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply(d, u, T, f, out, s));
+  }
   return PMG_OK;
 }
 
@@ -241,7 +263,12 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
       if (st) return st;
       rin = r;
     }
-    LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
+    if (h.fdm_path == 1) {
+      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_global(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
+      c->launches += 6;
+    } else {
+      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
+    }
     const bool emit = (it + 1 < steps) || traces_after;
     LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, emit ? T : nullptr, s));
   }

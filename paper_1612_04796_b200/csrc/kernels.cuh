@@ -35,6 +35,13 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
 bool apply_pipe_ok(const LevelDev &L);
 cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
                               double *out, const double *I, int nc, double *fc, cudaStream_t s);
+// global-memory paths for P = 32 blocks (windows > 32 or > shared memory); scratch X, Y: Ne*Mw;
+// apply: Cb = Ne*12n^2, V = Ne*n^3
+cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, double *Y, double *Z,
+                              cudaStream_t s);
+cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
+                                double *out, double *Cb, double *V, cudaStream_t s);
+bool fdm_mma_ok(const LevelDev &L);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
