@@ -37,6 +37,22 @@ def parse():
     return ap.parse_args()
 
 
+def max_over_ranks(x, device="cpu"):
+    """Max of a scalar over all ranks (the timing rule: a multi-GPU time is the slowest rank's)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(dofs_per_replica, world, cycles_per_replica, ms_max):
+    """Whole-job DOF/s of `world` independent replicas (weak scaling) timed by the slowest rank."""
+    return dofs_per_replica * world * cycles_per_replica / (ms_max / 1e3)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
         int(os.environ.get("LOCAL_RANK", 0))
@@ -137,18 +153,36 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # residual history (reduction per cycle) from the warm-up cycles
+    pcg = c.run == "pcg"
+    # residual history: V(1,1) cycles from u = 0 until ||r||/||r0|| <= 1e-10 (at most 30), or the
+    # PCG residual history (c5: V(1,1) as the preconditioner of inexact CG)
     r0 = float(np.sqrt(g.dot(f, f)))
-    hist = [r0]
-    for _ in range(args.warmup):
-        g.pmg_vcycle(u, f)
-        res = g.residual(u, f)
-        hist.append(float(np.sqrt(g.dot(res, res))))
+    if pcg:
+        _, hist, _ = g.pcg_solve(u, f, rtol=c.rtol, maxit=200)
+        hist = [float(x) for x in hist]
+    else:
+        hist = [r0]
+        for _ in range(30):
+            g.pmg_vcycle(u, f)
+            res = g.residual(u, f)
+            hist.append(float(np.sqrt(g.dot(res, res))))
+            if hist[-1] <= c.rtol * r0:
+                break
+        for _ in range(max(0, args.warmup - len(hist) + 1)):
+            g.pmg_vcycle(u, f)
     rho = [hist[i + 1] / hist[i] for i in range(len(hist) - 1)]
     u.zero_()
 
-    # ---- timed region: K cycles (CUDA-graph replay), device-timed with CUDA events on the
-    # launching stream; inputs > L2 for c3 (no flush)
+    def step():
+        if pcg:
+            u.zero_()
+            _, h, _ = g.pcg_solve(u, f, rtol=c.rtol, maxit=200)
+            return len(h) - 1
+        g.pmg_vcycle(u, f)
+        return 1
+
+    # ---- timed region: K steps (V-cycles replayed from CUDA graphs; for c5 K PCG solves),
+    # device-timed with CUDA events on the launching stream; inputs > L2 for c3 (no flush)
     clocks = ClockSampler(local_rank)
     g.profile(False)
     launches0 = g.launch_count()
@@ -157,57 +191,66 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    cycles = 0
     ev0.record(stream)
     for _ in range(args.steps):
-        g.pmg_vcycle(u, f)
+        cycles += step()
     ev1.record(stream)
     barrier()
     ms_total = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     launches = g.launch_count() - launches0
-    # ---- per-kernel CUDA-event timing of the same K cycles (eager launches, events on the
+    # ---- per-kernel CUDA-event timing of the same K steps (eager launches, events on the
     # launching stream around every kernel) -> the dominant kernel's roofline entry
     g.profile(True)
     g.profile_read(reset=True)
     barrier()
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
+    pcycles = 0
     p0.record(stream)
     for _ in range(args.steps):
-        g.pmg_vcycle(u, f)
+        pcycles += step()
     p1.record(stream)
     barrier()
     ms_profiled = p0.elapsed_time(p1) / args.steps
     prof = g.profile_read(reset=True)
     g.profile(False)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(ms_total, dev)
     ms_step = ms_total / args.steps
-    value = N * world * args.steps / (ms_total / 1e3)
+    # value: DOF/s per V(1,1) cycle (PCG: N * iterations / t, one V-cycle per iteration)
+    value = aggregate_value(N, world, cycles, ms_total)
 
     # ---- e2e: host buffers through the public API (H2D of u and f, cycle, D2H of u)
     u_host = torch.zeros(N, dtype=torch.float64).pin_memory()
     out_host = torch.empty(N, dtype=torch.float64).pin_memory()
-    for _ in range(2):
-        ud = u_host.to(dev, non_blocking=True)
-        fd = f_host.to(dev, non_blocking=True)
-        g.pmg_vcycle(ud, fd)
+    ud = torch.empty_like(u)
+    fd = torch.empty_like(f)
+
+    def e2e_step():
+        ud.copy_(u_host, non_blocking=True)
+        fd.copy_(f_host, non_blocking=True)
+        if pcg:
+            _, h, _ = g.pcg_solve(ud, fd, rtol=c.rtol, maxit=200)
+            k = len(h) - 1
+        else:
+            g.pmg_vcycle(ud, fd)
+            k = 1
         out_host.copy_(ud, non_blocking=True)
+        return k
+
+    for _ in range(2):
+        e2e_step()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    e2e_cycles = 0
     e0.record(stream)
     for _ in range(args.steps):
-        ud = u_host.to(dev, non_blocking=True)
-        fd = f_host.to(dev, non_blocking=True)
-        g.pmg_vcycle(ud, fd)
-        out_host.copy_(ud, non_blocking=True)
+        e2e_cycles += e2e_step()
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_ms = e0.elapsed_time(e1) / e2e_cycles
 
     # ---- roofline of the dominant kernel (Schwarz FDM solve on the top level)
     flops, bytes_, fdm_flops = cycle_model(g, c)
@@ -217,16 +260,20 @@ def run_ours(args, rank, world, local_rank):
     total_prof = sum(v[0] for v in prof.values())
     peak_tf = max(peak_dfma, peak_dmma)
     achieved_tf = fdm_flops / (fdm_avg_ms / 1e3) / 1e12 if fdm_avg_ms > 0 else None
-    kernels = {"%s@l%d" % k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+    kernels = {"%s@l%d" % k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
+                              "ms_per_cycle": round(v[0] / max(pcycles, 1), 4)}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     cyc_t_roof = max(flops / (peak_tf * 1e12), bytes_ / 6554.6e9)
     out = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "%s: %s, %dx%dx%d elements, P=%d %s, %d DOF, V(1,1) cycle"
+        "config": {"workload": "%s: %s, %dx%dx%d elements, P=%d %s, %d DOF, %s"
                    % (c.name, "periodic box %s" % (c.length,), c.ne[0], c.ne[1], c.ne[2], c.P,
-                      "GLL" if c.basis == 0 else "GL", N),
+                      "GLL" if c.basis == 0 else "GL", N,
+                      "step = one PCG solve to 1e-10 (one V(1,1) per iteration)" if pcg
+                      else "step = one V(1,1) cycle"),
+                   "cycles_timed": cycles,
                    "overlap": {"mode": c.overlap.mode, "value": c.overlap.value, "floor": c.overlap.floor},
                    "l2": "inputs larger than L2 (u, f, r: %.0f MB each); no flush" % (N * 8 / 1e6),
                    "parallelism": "replicas" if world > 1 else "single"},
@@ -242,8 +289,10 @@ def run_ours(args, rank, world, local_rank):
                                     "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = %.1f" % (
                                         peak_dfma, peak_dmma, FP64_NOMINAL_TFLOPS)},
         "cycle_roofline": {"flop_per_cycle": flops, "bytes_per_cycle": bytes_,
-                           "t_roof_ms": cyc_t_roof * 1e3, "frac": cyc_t_roof * 1e3 / ms_step},
+                           "t_roof_ms": cyc_t_roof * 1e3,
+                           "frac": cyc_t_roof * 1e3 / (ms_total / max(cycles, 1))},
         "residual_reduction_per_cycle": rho,
+        "residual_history": hist,
         "kernels": kernels,
         "ms_per_step_profiled_eager": ms_profiled,
         "clocks": clk,

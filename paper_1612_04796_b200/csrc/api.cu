@@ -248,7 +248,7 @@ int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *ou
 // `steps` Schwarz iterations.  traces_after: the last fold also emits the traces of the final u
 // (the caller's next operation is a residual of u on this level).
 int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool zero_init,
-                cudaStream_t s, bool traces_after = false) {
+                cudaStream_t s, bool traces_after = false, bool traces_ready = false) {
   LevelHost &h = c->lev[l];
   pmg::LevelDev d = level_dev(c, l);
   double *r = wsp<double>(c, h.o_r);
@@ -259,7 +259,7 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
     const bool zero = zero_init && it == 0;
     const double *rin = f;                       // u == 0  =>  r = f (Alg. 1 l.287-290)
     if (!zero) {
-      int st = residual_impl(c, l, u, f, r, s, it > 0);
+      int st = residual_impl(c, l, u, f, r, s, it > 0 || traces_ready);
       if (st) return st;
       rin = r;
     }
@@ -334,9 +334,17 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
   if ((st = coarse_impl(c, F[0], U[0], s))) return st;           // l.295
   for (int l = 1; l <= L; ++l) {                                  // l.298
     pmg::LevelDev d = level_dev(c, l);
-    LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, c->lev[l - 1].n, wsp<double>(c, c->lev[l].o_interp),
-                                  U[l - 1], U[l], s));            // l.299
-    if ((st = smooth_impl(c, l, U[l], F[l], c->nu2[l], false, s))) return st;  // l.301
+    const int nc = c->lev[l - 1].n;
+    const double *Il = wsp<double>(c, c->lev[l].o_interp);
+    bool tr = false;
+    if (c->nu2[l] > 0 && pmg::prolong_traces_ok(d, nc)) {          // l.299 + traces of u_l
+      LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong_traces(d, nc, Il, U[l - 1], U[l],
+                                                             wsp<double>(c, c->lev[l].o_T), s));
+      tr = true;
+    } else {
+      LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, nc, Il, U[l - 1], U[l], s));   // l.299
+    }
+    if ((st = smooth_impl(c, l, U[l], F[l], c->nu2[l], false, s, false, tr))) return st;  // l.301
   }
   return PMG_OK;
 }

@@ -642,6 +642,59 @@ __global__ void __launch_bounds__(512, 1) k_apply_pipe(LevelDev L, const double 
   cp_async_wait<0>();
 }
 
+// Fused correction prolongation + face traces (Alg. 1 l.299 followed by the trace pass of the
+// post-smoothing residual): u_f += (I (x) I (x) I) u_c with three DMMA line GEMMs in shared
+// memory, u_f written back, and the traces of the new u_f emitted for the residual.
+// smem: Uc (nc^3) | T1 (nf nc^2) | T2 (nf^2 nc) | U (nf^3) | trs (12 nf)
+__global__ void __launch_bounds__(256) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
+                                                        const double *__restrict__ uc,
+                                                        double *__restrict__ uf,
+                                                        double *__restrict__ T) {
+  extern __shared__ double sm[];
+  const int nf = L.n, n2 = nf * nf, n3 = n2 * nf;
+  const int c3 = nc * nc * nc;
+  double *Uc = sm, *T1 = Uc + c3, *T2 = T1 + nf * nc * nc, *U = T2 + nf * nf * nc, *trs = U + n3;
+  const int e = blockIdx.x;
+  stage(Uc, uc + (long long)e * c3, c3);
+  stage(U, uf + (long long)e * n3, n3);
+  for (int d = 0; d < 3; ++d) stage(trs + d * 4 * nf, L.tr[d], 4 * nf);
+  cp_async_wait_all();
+  __syncthreads();
+  const Blk BC = {{nc, nc, nc}, {1, nc, nc * nc}};
+  const Blk B1 = {{nf, nc, nc}, {1, nf, nf * nc}};
+  const Blk B2 = {{nf, nf, nc}, {1, nf, nf * nf}};
+  const Blk BF = {{nf, nf, nf}, {1, nf, n2}};
+  const LineSpec px = {nf, nc, I, nc, 1, nullptr, 0, 0, 0, 0};   // A[o][k] = I[o*nc + k]
+  EpiStore s1{T1, B1};
+  mma_lines_gen<0>(Uc, BC, px, s1); __syncthreads();
+  EpiStore s2{T2, B2};
+  mma_lines_gen<1>(T1, B1, px, s2); __syncthreads();
+  EpiAcc acc{U, BF, false};
+  mma_lines_gen<2>(T2, B2, px, acc); __syncthreads();
+  double *ue = uf + (long long)e * n3;
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % nf, p1 = p / nf;
+    int base, stride;
+    if (d == 0) { base = nf * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = nf; }
+    else { base = p0 + nf * p1; stride = n2; }
+    const double *tr = trs + d * 4 * nf;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < nf; ++i) {
+      const double v = U[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[nf + i] * v;
+      lv += tr[2 * nf + i] * v;
+      lder += tr[3 * nf + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Global-memory (L2-resident) batched line GEMMs for blocks too large for shared memory
 // (P = 32: 33^3 elements, 45^3 Schwarz windows).  Every warp grabs (block, 8-column tile,
@@ -1400,6 +1453,27 @@ cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double
     if (e) return e;
   }
   k_mass_finish<<<grid_for((long long)L.Ne * bs, 256), 256, 0, s>>>(L, V, f, out);
+  return cudaGetLastError();
+}
+
+static size_t prolong_traces_smem(int nf, int nc) {
+  return sizeof(double) * ((size_t)nc * nc * nc + (size_t)nf * nc * nc + (size_t)nf * nf * nc +
+                           (size_t)nf * nf * nf + 12 * (size_t)nf);
+}
+
+bool prolong_traces_ok(const LevelDev &Lf, int nc) {
+  return Lf.n <= 17 && prolong_traces_smem(Lf.n, nc) <= 200 * 1024;
+}
+
+cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                                  double *uf, double *T, cudaStream_t s) {
+  const size_t sb = prolong_traces_smem(Lf.n, nc);
+  static size_t configured = 0;
+  if (sb > 48 * 1024 && sb > configured) {
+    cudaFuncSetAttribute(k_prolong_traces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    configured = sb;
+  }
+  k_prolong_traces<<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
   return cudaGetLastError();
 }
 

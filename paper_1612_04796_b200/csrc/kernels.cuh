@@ -42,6 +42,10 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
 cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
                                 double *out, double *Cb, double *V, cudaStream_t s);
 bool fdm_mma_ok(const LevelDev &L);
+// fused prolongation u_f += I u_c + traces of the new u_f (n_f <= 17)
+bool prolong_traces_ok(const LevelDev &Lf, int nc);
+cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                                  double *uf, double *T, cudaStream_t s);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
