@@ -293,11 +293,11 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
 
 // Supported (KS, MT) tiles; any request is served by the smallest supported tile that covers
 // it (A is zero padded, so a larger tile is correct, only wasteful).
-template <int DIR, class Epi>
+template <int DIR, int KSMAX, class Epi>
 __device__ void mma_lines_gen(const double *X, const Blk &B, const LineSpec &ls, Epi &epi) {
   const int KS = (ls.mk + ls.next + 3) >> 2, MT = (ls.mo + 7) >> 3;
 #define PMG_TILE(ks, mt) \
-  if (KS <= ks && MT <= mt) { mma_lines_t<DIR, ks, mt>(X, B, ls, epi); return; }
+  if (ks <= KSMAX && KS <= ks && MT <= mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt>(X, B, ls, epi); return; }
   PMG_TILE(1, 1) PMG_TILE(2, 1) PMG_TILE(2, 2) PMG_TILE(3, 1) PMG_TILE(3, 2) PMG_TILE(3, 3)
   PMG_TILE(4, 2) PMG_TILE(5, 2) PMG_TILE(5, 3) PMG_TILE(6, 3) PMG_TILE(7, 4) PMG_TILE(8, 4)
 #undef PMG_TILE
@@ -305,11 +305,11 @@ __device__ void mma_lines_gen(const double *X, const Blk &B, const LineSpec &ls,
 }
 
 // square contraction (FDM passes): A[o][k] = Amat[o*ao + k*ak], mo = mk = extent along DIR
-template <int DIR, class Epi>
+template <int DIR, int KSMAX, class Epi>
 __device__ __forceinline__ void mma_lines_dispatch(const double *X, const Blk &B, const double *Amat,
                                                    int ao, int ak, Epi &epi) {
   const LineSpec ls = {B.m[DIR], B.m[DIR], Amat, ao, ak, nullptr, 0, 0, 0, 0};
-  mma_lines_gen<DIR>(X, B, ls, epi);
+  mma_lines_gen<DIR, KSMAX>(X, B, ls, epi);
 }
 
 template <int DIR>
@@ -369,7 +369,8 @@ struct EpiMassAcc {
 };
 
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
-__global__ void __launch_bounds__(256, 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
+template <int KSMAX>
+__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
                                                  double *__restrict__ Z) {
   extern __shared__ double sm[];
   const int n = L.n, n3 = n * n * n;
@@ -430,20 +431,21 @@ __global__ void __launch_bounds__(256, 2) k_fdm_mma(LevelDev L, const double *__
   EpiDivide dv{X, B, {lam[0], lam[1], lam[2]}};
   EpiWeightStore ws{Z + (long long)e * Mw, B, {W[0], W[1], W[2]}};
   // forward: A = S^T, i.e. A[o][k] = S[k*m + o]
-  mma_lines_dispatch<0>(X, B, Ss[0], 1, m[0], st); __syncthreads();
-  mma_lines_dispatch<1>(X, B, Ss[1], 1, m[1], st); __syncthreads();
-  mma_lines_dispatch<2>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
+  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], 1, m[0], st); __syncthreads();
+  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], 1, m[1], st); __syncthreads();
+  mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
   // backward: A = S
-  mma_lines_dispatch<2>(X, B, Ss[2], m[2], 1, st); __syncthreads();
-  mma_lines_dispatch<1>(X, B, Ss[1], m[1], 1, st); __syncthreads();
-  mma_lines_dispatch<0>(X, B, Ss[0], m[0], 1, ws);
+  mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], m[2], 1, st); __syncthreads();
+  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], m[1], 1, st); __syncthreads();
+  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
 }
 
 // smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
 // Per direction d the line GEMM is  V += M_p M_q [D | a ap b bp] [U-lines ; c1 c2 c3 c4]  where
 // c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
 // c1 = -tdR/2 - mu tvR, c2 = tvR/2, c3 = tdL/2 - mu tvL, c4 = -tvL/2.
-__global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+template <int KSMAX>
+__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
                                                       const double *__restrict__ T,
                                                       const double *__restrict__ f,
                                                       double *__restrict__ out,
@@ -483,12 +485,12 @@ __global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *
   const Blk B = {{n, n, n}, {1, n, n2}};
   EpiAcc acc{V, B, true};
   LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
-  mma_lines_gen<0>(U, B, lx, acc); __syncthreads();
+  mma_lines_gen<0, KSMAX>(U, B, lx, acc); __syncthreads();
   acc.first = false;
   LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
-  mma_lines_gen<1>(U, B, ly, acc); __syncthreads();
+  mma_lines_gen<1, KSMAX>(U, B, ly, acc); __syncthreads();
   LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
-  mma_lines_gen<2>(U, B, lz, acc); __syncthreads();
+  mma_lines_gen<2, KSMAX>(U, B, lz, acc); __syncthreads();
   // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism
   const long long g0 = (long long)e * n3;
   constexpr int UNR = 4;
@@ -519,134 +521,20 @@ __global__ void __launch_bounds__(256, 2) k_apply_mma(LevelDev L, const double *
     const Blk FC = {{nc, nc, nc}, {1, nc, nc * nc}};
     const LineSpec rx = {nc, n, restrict_I, 1, nc, nullptr, 0, 0, 0, 0};
     EpiStore s1{U, T1};
-    mma_lines_gen<0>(V, B, rx, s1); __syncthreads();
+    mma_lines_gen<0, KSMAX>(V, B, rx, s1); __syncthreads();
     EpiStore s2{Cf, T2};
-    mma_lines_gen<1>(U, T1, rx, s2); __syncthreads();
+    mma_lines_gen<1, KSMAX>(U, T1, rx, s2); __syncthreads();
     EpiStore s3{fc + (long long)e * nc * nc * nc, FC};
-    mma_lines_gen<2>(Cf, T2, rx, s3);
+    mma_lines_gen<2, KSMAX>(Cf, T2, rx, s3);
   }
-}
-
-// Persistent, double-buffered operator apply / residual (+ optional fused restriction).
-// One CTA per SM walks elements e = blockIdx.x, +gridDim.x, ...; while element e is computed
-// from buffer b, the cp.async loads of the next element (u block and neighbour face traces)
-// stream into buffer b^1, so HBM stays busy.  Per element: V = sum_d line-GEMM_d (augmented
-// K, see k_apply_mma), then r = f - M V (or M V) to global, or -- with `restrict_I` -- r stays in
-// shared memory and f_c = I^T r is computed by three more line GEMMs and written to the
-// coarse level (Alg. 1 l.292 fused: no global r).
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void apply_issue_loads(const LevelDev &L, int e, const double *u,
-                                                  const double *T, double *U, double *Cf) {
-  const int n = L.n, n2 = n * n, n3 = n2 * n;
-  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
-  const int ecoord[3] = {ex, ey, ez};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  stage(U, u + (long long)e * n3, n3);
-  for (int d = 0; d < 3; ++d) {
-    int c[3] = {ex, ey, ez};
-    c[d] = wrap(ecoord[d] + 1, edim[d]);
-    stage(Cf + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
-          2 * n2);
-    c[d] = wrap(ecoord[d] - 1, edim[d]);
-    stage(Cf + d * 4 * n2 + 2 * n2,
-          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
-  }
-}
-
-// smem: U[2] (n^3 each) | Cf[2] (12 n^2 each) | V (n^3) | mass (3n)
-__global__ void __launch_bounds__(512, 1) k_apply_pipe(LevelDev L, const double *__restrict__ u,
-                                                       const double *__restrict__ T,
-                                                       const double *__restrict__ f,
-                                                       double *__restrict__ out,
-                                                       const double *__restrict__ restrict_I,
-                                                       int nc, double *__restrict__ fc) {
-  extern __shared__ double sm[];
-  const int n = L.n, n2 = n * n, n3 = n2 * n;
-  double *Ub[2] = {sm, sm + n3};
-  double *Cb[2] = {sm + 2 * n3, sm + 2 * n3 + 12 * n2};
-  double *V = sm + 2 * n3 + 24 * n2;
-  double *ms = V + n3;
-  for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
-  int e = blockIdx.x;
-  if (e < L.Ne) apply_issue_loads(L, e, u, T, Ub[0], Cb[0]);
-  cp_async_commit();
-  int b = 0;
-  const Blk B = {{n, n, n}, {1, n, n2}};
-  for (; e < L.Ne; e += gridDim.x) {
-    const int en = e + gridDim.x;
-    if (en < L.Ne) apply_issue_loads(L, en, u, T, Ub[b ^ 1], Cb[b ^ 1]);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    double *U = Ub[b], *Cf = Cb[b];
-    for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-      const int d = t / n2, pp = t - d * n2;
-      double *C = Cf + d * 4 * n2 + pp;
-      const double mu = L.mu[d];
-      const double tvR = C[0], tdR = C[n2], tvL = C[2 * n2], tdL = C[3 * n2];
-      C[0] = -0.5 * tdR - mu * tvR;
-      C[n2] = 0.5 * tvR;
-      C[2 * n2] = 0.5 * tdL - mu * tvL;
-      C[3 * n2] = -0.5 * tvL;
-    }
-    __syncthreads();
-    EpiAcc acc{V, B, true};
-    LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
-    mma_lines_gen<0>(U, B, lx, acc); __syncthreads();
-    acc.first = false;
-    LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
-    mma_lines_gen<1>(U, B, ly, acc); __syncthreads();
-    LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
-    mma_lines_gen<2>(U, B, lz, acc); __syncthreads();
-    const long long g0 = (long long)e * n3;
-    constexpr int UNR = 4;
-    for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
-      double fv[UNR];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int t = t0 + q * blockDim.x;
-        fv[q] = (f && t < n3) ? __ldg(f + g0 + t) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int t = t0 + q * blockDim.x;
-        if (t >= n3) break;
-        const int i = t % n, j = (t / n) % n, k = t / n2;
-        const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
-        const double rr = f ? fv[q] - v : v;
-        if (restrict_I) V[t] = rr;
-        else out[g0 + t] = rr;
-      }
-    }
-    if (restrict_I) {
-      __syncthreads();
-      // f_c = (I^T (x) I^T (x) I^T) r: x (n -> nc) into U, y into Cf, z to global
-      const Blk R = B;
-      const Blk T1 = {{nc, n, n}, {1, nc, nc * n}};
-      const Blk T2 = {{nc, nc, n}, {1, nc, nc * nc}};
-      const Blk FC = {{nc, nc, nc}, {1, nc, nc * nc}};
-      EpiStore s1{U, T1};
-      LineSpec rx = {nc, n, restrict_I, 1, nc, nullptr, 0, 0, 0, 0};
-      mma_lines_gen<0>(V, R, rx, s1); __syncthreads();
-      EpiStore s2{Cf, T2};
-      mma_lines_gen<1>(U, T1, rx, s2); __syncthreads();
-      EpiStore s3{fc + (long long)e * nc * nc * nc, FC};
-      mma_lines_gen<2>(Cf, T2, rx, s3);
-    }
-    __syncthreads();
-    b ^= 1;
-  }
-  cp_async_wait<0>();
 }
 
 // Fused correction prolongation + face traces (Alg. 1 l.299 followed by the trace pass of the
 // post-smoothing residual): u_f += (I (x) I (x) I) u_c with three DMMA line GEMMs in shared
 // memory, u_f written back, and the traces of the new u_f emitted for the residual.
 // smem: Uc (nc^3) | T1 (nf nc^2) | T2 (nf^2 nc) | U (nf^3) | trs (12 nf)
-__global__ void __launch_bounds__(256) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
+template <int KSMAX>
+__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
                                                         const double *__restrict__ uc,
                                                         double *__restrict__ uf,
                                                         double *__restrict__ T) {
@@ -666,11 +554,11 @@ __global__ void __launch_bounds__(256) k_prolong_traces(LevelDev L, int nc, cons
   const Blk BF = {{nf, nf, nf}, {1, nf, n2}};
   const LineSpec px = {nf, nc, I, nc, 1, nullptr, 0, 0, 0, 0};   // A[o][k] = I[o*nc + k]
   EpiStore s1{T1, B1};
-  mma_lines_gen<0>(Uc, BC, px, s1); __syncthreads();
+  mma_lines_gen<0, KSMAX>(Uc, BC, px, s1); __syncthreads();
   EpiStore s2{T2, B2};
-  mma_lines_gen<1>(T1, B1, px, s2); __syncthreads();
+  mma_lines_gen<1, KSMAX>(T1, B1, px, s2); __syncthreads();
   EpiAcc acc{U, BF, false};
-  mma_lines_gen<2>(T2, B2, px, acc); __syncthreads();
+  mma_lines_gen<2, KSMAX>(T2, B2, px, acc); __syncthreads();
   double *ue = uf + (long long)e * n3;
   for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
   double *Te = T + (long long)e * 12 * n2;
@@ -955,96 +843,6 @@ __global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restr
     }
     const long long g = (long long)e * n3 + t;
     u[g] = zero ? du : u[g] + du;
-  }
-}
-
-// Shared-memory fold (Eq. 10 scatter, deterministic): the element's DOFs are staged in shared
-// memory, the weighted corrections of the 27 subdomains whose windows touch this element are
-// added sub-box by sub-box in a fixed order (own subdomain first, then the 26 neighbours),
-// u is written back coalesced and, optionally, the face traces of the updated u are emitted
-// (fusing the trace kernel of the following residual).
-__device__ __forceinline__ int src_off(int code) { return code == 0 ? 0 : (code == 1 ? -1 : 1); }
-
-__global__ void __launch_bounds__(256) k_fold_sm(LevelDev L, const double *__restrict__ Z,
-                                                 double *__restrict__ u, int zero,
-                                                 double *__restrict__ T) {
-  extern __shared__ double sm[];
-  const int n = L.n, n2 = n * n, n3 = n2 * n;
-  const int mx = L.m[0], my = L.m[1], Mw = L.Mw;
-  double *U = sm, *trs = sm + n3;
-  const int e = blockIdx.x;
-  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  if (zero) {
-    for (int t = threadIdx.x; t < n3; t += blockDim.x) U[t] = 0.0;
-  } else {
-    stage(U, u + (long long)e * n3, n3);
-  }
-  if (T)
-    for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
-  cp_async_wait_all();
-  __syncthreads();
-  for (int src = 0; src < 27; ++src) {
-    const int oc[3] = {src % 3, (src / 3) % 3, src / 9};
-    int lo[3], cnt[3], woff[3], sc[3];
-    bool empty = false;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int no = L.no[d], o = src_off(oc[d]);
-      if (o == 0) { lo[d] = 0; cnt[d] = n; woff[d] = no; }
-      else if (o == -1) { lo[d] = 0; cnt[d] = no; woff[d] = no + n; }   // e is the right nb of s
-      else { lo[d] = n - no; cnt[d] = no; woff[d] = no - n; }           // e is the left nb of s
-      empty |= cnt[d] == 0;
-      sc[d] = wrap(ec[d] + o, edim[d]);
-    }
-    if (empty) continue;
-    const double *Zs = Z + (long long)(sc[0] + L.nx * (sc[1] + L.ny * sc[2])) * Mw;
-    const int total = cnt[0] * cnt[1] * cnt[2];
-    constexpr int UNR = 4;
-    for (int w0 = threadIdx.x; w0 < total; w0 += UNR * blockDim.x) {
-      double zv[UNR];
-      int li[UNR];
-#pragma unroll
-      for (int q = 0; q < UNR; ++q) {
-        const int w = w0 + q * blockDim.x;
-        li[q] = -1;
-        zv[q] = 0.0;
-        if (w < total) {
-          const int a = w % cnt[0], r = w / cnt[0];
-          const int b = r % cnt[1], c = r / cnt[1];
-          const int i = lo[0] + a, j = lo[1] + b, k = lo[2] + c;
-          li[q] = i + n * (j + n * k);
-          zv[q] = __ldg(Zs + (woff[0] + i) + mx * ((woff[1] + j) + my * (woff[2] + k)));
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < UNR; ++q)
-        if (li[q] >= 0) U[li[q]] += zv[q];
-    }
-    __syncthreads();
-  }
-  double *ue = u + (long long)e * n3;
-  for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
-  if (!T) return;
-  double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int i = 0; i < n; ++i) {
-      const double v = U[base + i * stride];
-      rv += tr[i] * v;
-      rder += tr[n + i] * v;
-      lv += tr[2 * n + i] * v;
-      lder += tr[3 * n + i] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
   }
 }
 
@@ -1401,6 +1199,23 @@ cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStr
   }
   return cudaGetLastError();
 }
+// allow up to 227 KB of dynamic shared memory for every shared-memory kernel variant (once)
+static void configure_smem() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const int mx = 227 * 1024;
+  cudaFuncSetAttribute(k_fdm_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_fdm_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_fdm_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_prolong_traces<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_prolong_traces<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_prolong_traces<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
 static int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -1467,13 +1282,11 @@ bool prolong_traces_ok(const LevelDev &Lf, int nc) {
 
 cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, const double *uc,
                                   double *uf, double *T, cudaStream_t s) {
+  configure_smem();
   const size_t sb = prolong_traces_smem(Lf.n, nc);
-  static size_t configured = 0;
-  if (sb > 48 * 1024 && sb > configured) {
-    cudaFuncSetAttribute(k_prolong_traces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    configured = sb;
-  }
-  k_prolong_traces<<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
+  if (((nc + 3) >> 2) <= 2) k_prolong_traces<2><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
+  else if (((nc + 3) >> 2) <= 4) k_prolong_traces<4><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
+  else k_prolong_traces<8><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
   return cudaGetLastError();
 }
 
@@ -1484,13 +1297,12 @@ static size_t apply_mma_smem(int n) {
 
 cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
                               double *out, const double *I, int nc, double *fc, cudaStream_t s) {
+  configure_smem();
   const size_t sb = apply_mma_smem(L.n);
-  static size_t configured = 0;
-  if (sb > 48 * 1024 && sb > configured) {
-    cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    configured = sb;
-  }
-  k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  const int ks = (L.n + 4 + 3) >> 2;
+  if (ks <= 2) k_apply_mma<2><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  else if (ks <= 4) k_apply_mma<4><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  else k_apply_mma<8><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
   return cudaGetLastError();
 }
 
@@ -1498,15 +1310,8 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
                          double *out, cudaStream_t s) {
   const int n = L.n;
 
-  if (n <= 20) {
-    const size_t n2 = (size_t)n * n, n3 = n2 * n;
-    const size_t sb = sizeof(double) * (2 * n3 + 12 * n2 + 3 * n);
-    static size_t configured = 0;
-    if (sb > 48 * 1024 && sb > configured) {
-      cudaFuncSetAttribute(k_apply_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-      configured = sb;
-    }
-    k_apply_mma<<<L.Ne, 256, sb, s>>>(L, u, T, f, out, nullptr, 0, nullptr);
+  if (n <= 17) {
+    return launch_apply_pipe(L, u, T, f, out, nullptr, 0, nullptr, s);
   } else {
     k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
   }
@@ -1525,13 +1330,12 @@ bool fdm_mma_ok(const LevelDev &L) {
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s) {
   if (fdm_mma_ok(L)) {
+    configure_smem();
     const size_t sb = fdm_mma_smem_bytes(L);
-    static size_t configured = 0;
-    if (sb > 48 * 1024 && sb > configured) {
-      cudaFuncSetAttribute(k_fdm_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-      configured = sb;
-    }
-    k_fdm_mma<<<L.Ne, 256, sb, s>>>(L, r, Z);
+    const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
+    if (ks <= 2) k_fdm_mma<2><<<L.Ne, 256, sb, s>>>(L, r, Z);
+    else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 256, sb, s>>>(L, r, Z);
+    else k_fdm_mma<8><<<L.Ne, 256, sb, s>>>(L, r, Z);
     return cudaGetLastError();
   }
   if (smem) {
