@@ -368,6 +368,95 @@ struct EpiMassAcc {
   }
 };
 
+// Fused z passes of the fast diagonalisation: forward S_z^T, eigen-divide, backward S_z on the
+// same z columns.  A warp owns its columns through both GEMMs, so no block barrier is needed
+// between them (only __syncwarp around the in-place round trip through shared memory).
+template <int KS, int MT>
+__device__ __forceinline__ void fdm_z_fused_t(double *X, const Blk &B, const double *S,
+                                              const double *const *lam) {
+  const int md = B.m[2], mp = B.m[0], mq = B.m[1];
+  const int ncol = mp * mq;
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)mp + 1u;
+  const int so = B.s[2], sq = B.s[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double af[MT][KS], ab[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      const bool ok = o < md && k < md;
+      af[mt][ks] = ok ? S[k * md + o] : 0.0;
+      ab[mt][ks] = ok ? S[o * md + k] : 0.0;
+    }
+  int koff[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) koff[ks] = min(ks * 4 + t, md - 1) * so;
+  const int ntiles = (ncol + 7) >> 3;
+  for (int tile = warp; tile < ntiles; tile += nw) {
+    const int nb = min(tile * 8 + g, ncol - 1);
+    const int qb = __umulhi((unsigned)nb, magic), pb = nb - qb * mp;
+    const double *xb = X + pb + qb * sq;
+    double b[KS], c[MT][2];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = xb[koff[ks]];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], af[mt][ks], b[ks]);
+    __syncwarp();
+    int wb[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tile * 8 + 2 * t + j;
+      wb[j] = -1;
+      if (n >= ncol) continue;
+      const int q = __umulhi((unsigned)n, magic), p = n - q * mp;
+      wb[j] = p + q * sq;
+      const double cf = lam[0][p] + lam[1][q];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o < md) X[wb[j] + o * so] = c[mt][j] * rcp_nr(cf + lam[2][o]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = xb[koff[ks]];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], ab[mt][ks], b[ks]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (wb[j] < 0) continue;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o < md) X[wb[j] + o * so] = c[mt][j];
+      }
+    }
+  }
+}
+
+// returns false if the window is too large for the fused register budget (caller falls back)
+template <int KSMAX>
+__device__ __forceinline__ bool fdm_z_fused(double *X, const Blk &B, const double *S,
+                                            const double *const *lam) {
+  const int KS = (B.m[2] + 3) >> 2;
+  if (KS <= 1) { fdm_z_fused_t<1, 1>(X, B, S, lam); return true; }
+  if (KS <= 2) { fdm_z_fused_t<2, 1>(X, B, S, lam); return true; }
+  if (KSMAX >= 4 && KS <= 4) { fdm_z_fused_t<(KSMAX >= 4 ? 4 : 1), 2>(X, B, S, lam); return true; }
+  if (KSMAX >= 6 && KS <= 6) { fdm_z_fused_t<(KSMAX >= 6 ? 6 : 1), 3>(X, B, S, lam); return true; }
+  return false;
+}
+
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
 template <int KSMAX>
 __global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
@@ -433,9 +522,13 @@ __global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_fdm_mma(LevelDev L,
   // forward: A = S^T, i.e. A[o][k] = S[k*m + o]
   mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], 1, m[0], st); __syncthreads();
   mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], 1, m[1], st); __syncthreads();
-  mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
-  // backward: A = S
-  mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], m[2], 1, st); __syncthreads();
+  const double *lamc[3] = {lam[0], lam[1], lam[2]};
+  if (!fdm_z_fused<KSMAX>(X, B, Ss[2], lamc)) {
+    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
+    // backward: A = S
+    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], m[2], 1, st);
+  }
+  __syncthreads();
   mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], m[1], 1, st); __syncthreads();
   mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
 }
@@ -1015,36 +1108,32 @@ __global__ void k_coarse_xf(CoarseDev C, int nx, int ny, const double *__restric
   }
 }
 
-// z column: forward S_z^T, divide by the eigenvalue sums (null mode -> 0), backward S_z
-template <int GMAX>
+// z column (one warp per column, lane = z index): forward S_z^T, divide by the eigenvalue
+// sums (null mode -> 0), backward S_z; column values exchanged with warp shuffles.
 __global__ void k_coarse_z(CoarseDev C, double *__restrict__ G) {
   const int Gx = C.G[0], Gy = C.G[1], Gz = C.G[2];
   const long long cols = (long long)Gx * Gy;
-  const long long st = cols;
-  for (long long cidx = blockIdx.x * (long long)blockDim.x + threadIdx.x; cidx < cols;
-       cidx += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const double *S = C.S[2];
+  for (long long cidx = w0; cidx < cols; cidx += nw) {
     const int a = cidx % Gx, b = cidx / Gx;
-    double v[GMAX], w[GMAX];
-#pragma unroll
-    for (int k = 0; k < GMAX; ++k) v[k] = k < Gz ? G[cidx + k * st] : 0.0;
-#pragma unroll
-    for (int o = 0; o < GMAX; ++o) {
-      double acc = 0;
-#pragma unroll
-      for (int k = 0; k < GMAX; ++k)
-        if (k < Gz && o < Gz) acc += C.S[2][k * Gz + o] * v[k];
-      const double den = C.lam[0][a] + C.lam[1][b] + (o < Gz ? C.lam[2][o] : 1.0);
-      w[o] = (a == 0 && b == 0 && o == 0) ? 0.0 : acc / den;
+    const double v = lane < Gz ? G[cidx + lane * cols] : 0.0;
+    double acc = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double vk = __shfl_sync(0xffffffffu, v, k);
+      if (lane < Gz) acc += S[k * Gz + lane] * vk;
     }
-#pragma unroll
-    for (int o = 0; o < GMAX; ++o) {
-      if (o >= Gz) break;
-      double acc = 0;
-#pragma unroll
-      for (int k = 0; k < GMAX; ++k)
-        if (k < Gz) acc += C.S[2][o * Gz + k] * w[k];
-      G[cidx + o * st] = acc;
+    double w = 0.0;
+    if (lane < Gz && !(a == 0 && b == 0 && lane == 0))
+      w = acc / (C.lam[0][a] + C.lam[1][b] + C.lam[2][lane]);
+    double out = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double wk = __shfl_sync(0xffffffffu, w, k);
+      if (lane < Gz) out += S[lane * Gz + k] * wk;
     }
+    if (lane < Gz) G[cidx + lane * cols] = out;
   }
 }
 
@@ -1407,10 +1496,8 @@ cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const do
   const long long cols = (long long)C.G[0] * C.G[1];
   k_coarse_xf<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, f0, G1);
   k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 1, G1, G2);
-  if (C.G[2] <= 8) k_coarse_z<8><<<grid_for(cols, 128), 128, 0, s>>>(C, G2);
-  else if (C.G[2] <= 16) k_coarse_z<16><<<grid_for(cols, 128), 128, 0, s>>>(C, G2);
-  else if (C.G[2] <= 32) k_coarse_z<32><<<grid_for(cols, 128), 128, 0, s>>>(C, G2);
-  else return cudaErrorInvalidValue;
+  if (C.G[2] > 32) return cudaErrorInvalidValue;
+  k_coarse_z<<<grid_for(cols * 32, 256), 256, 0, s>>>(C, G2);
   k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 0, G2, G1);
   k_coarse_xb<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, G1, u0);
   return cudaGetLastError();
