@@ -21,6 +21,9 @@ __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ void stage(double *dst, const double *src, int count) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) cp_async8(dst + i, src + i);
 }
@@ -455,6 +458,61 @@ __device__ __forceinline__ bool fdm_z_fused(double *X, const Blk &B, const doubl
   if (KSMAX >= 4 && KS <= 4) { fdm_z_fused_t<(KSMAX >= 4 ? 4 : 1), 2>(X, B, S, lam); return true; }
   if (KSMAX >= 6 && KS <= 6) { fdm_z_fused_t<(KSMAX >= 6 ? 6 : 1), 3>(X, B, S, lam); return true; }
   return false;
+}
+
+// ---- building blocks of the subdomain solve (shared by the one-shot and persistent kernels)
+// gather offsets of subdomain e: global address of window node (a,b,c) = xo[a] + yo[b] + zo[c]
+__device__ __forceinline__ void fdm_offsets(const LevelDev &L, int e, long long *offs) {
+  const int n = L.n, n3 = n * n * n;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  const long long estride[3] = {(long long)n3, (long long)L.nx * n3, (long long)L.nx * L.ny * n3};
+  const int lstride[3] = {1, n, n * n};
+  int base = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int no = L.no[d];
+    for (int a = threadIdx.x; a < L.m[d]; a += blockDim.x) {
+      const int o = a < no ? -1 : (a < no + n ? 0 : 1);
+      const int li = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
+      offs[base + a] = wrap(ec[d] + o, edim[d]) * estride[d] + li * lstride[d];
+    }
+    base += L.m[d];
+  }
+}
+
+__device__ __forceinline__ void fdm_gather(const LevelDev &L, const double *r, const long long *offs,
+                                           double *X) {
+  const int m0 = L.m[0], m1 = L.m[1];
+  const long long *xo = offs, *yo = offs + m0, *zo = offs + m0 + m1;
+  const int total = L.Mw;
+  int a = threadIdx.x % m0, bc = threadIdx.x / m0;
+  int b = bc % m1, c = bc / m1;
+  const int da = blockDim.x % m0, dbc = blockDim.x / m0;
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    cp_async8(X + w, r + xo[a] + yo[b] + zo[c]);
+    a += da; b += dbc;
+    if (a >= m0) { a -= m0; ++b; }
+    while (b >= m1) { b -= m1; ++c; }
+  }
+}
+
+template <int KSMAX>
+__device__ __forceinline__ void fdm_phases(double *X, const int *m, double *const *Ss,
+                                           const double *const *lam, const double *const *W,
+                                           double *Ze) {
+  const Blk B = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};
+  EpiStore st{X, B};
+  EpiDivide dv{X, B, {lam[0], lam[1], lam[2]}};
+  EpiWeightStore ws{Ze, B, {W[0], W[1], W[2]}};
+  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], 1, m[0], st); __syncthreads();
+  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], 1, m[1], st); __syncthreads();
+  if (!fdm_z_fused<KSMAX>(X, B, Ss[2], lam)) {
+    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
+    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], m[2], 1, st);
+  }
+  __syncthreads();
+  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], m[1], 1, st); __syncthreads();
+  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
 }
 
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
