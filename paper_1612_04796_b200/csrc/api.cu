@@ -164,7 +164,7 @@ void plan_workspace(dg_ctx *c) {
         mmax = std::max(mmax, h.m[d]);
       }
       if (mmax <= 32 && mma_words * sizeof(double) <= FDM_SMEM_MAX) h.fdm_path = 0;
-      else if (mmax <= 48) h.fdm_path = 1;
+      else if (mmax <= 80) h.fdm_path = 1;
       else h.fdm_path = 2;
       const size_t sb = sizeof(double) * (2 * (size_t)h.Mw);
       h.fdm_smem = sb <= FDM_SMEM_MAX;

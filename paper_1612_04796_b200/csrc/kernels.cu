@@ -856,6 +856,7 @@ cudaError_t lines_global(const double *X, long long xbs, const Blk &B, const Lin
   const int grid = 148 * 8;
   if (KS <= 6) k_lines_global<DIR, 6, 3, Epi><<<grid, 256, 0, s>>>(X, xbs, B, ls, ebs, nblocks, epi);
   else if (KS <= 12) k_lines_global<DIR, 12, 3, Epi><<<grid, 256, 0, s>>>(X, xbs, B, ls, ebs, nblocks, epi);
+  else if (KS <= 20) k_lines_global<DIR, 20, 1, Epi><<<grid, 256, 0, s>>>(X, xbs, B, ls, ebs, nblocks, epi);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

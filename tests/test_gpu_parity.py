@@ -232,3 +232,36 @@ def test_errors_fail_loudly():
         g.pmg_vcycle(u, u)                  # no Schwarz setup / aliased
     with pytest.raises(PMGError):
         g.apply(u, out=u)                   # aliased
+
+
+# ---- NEXT rows: variable V-cycle (Table 2) and the large-window global path
+def test_variable_vcycle_schedule():
+    c = get_config("c2", 3)
+    g = _gpu(c)
+    H = _oracle(c)
+    nu = [0] + [3 ** (H.L - l) for l in range(1, H.L + 1)]      # (1,1) x 3^(L-l)
+    g.set_schedule(nu, nu)
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    g.pmg_vcycle(ug, _t(f))
+    assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f, growth=3)) <= TOL
+
+
+BIG = [
+    Config("e-gll05-p16", (3, 3, 3), (1.0, 1.0, 1.0), 16, 0, OverlapSpec(1, 0.5, 0)),     # m = 35
+    Config("e-full-p16", (3, 3, 4), (1.0, 1.0, 1.3), 16, 0, OverlapSpec(0, 17, 0)),      # m = 51
+]
+
+
+@pytest.mark.parametrize("c", BIG, ids=[e.name for e in BIG])
+def test_large_windows_global_path(c):
+    g = _gpu(c)
+    H = MFHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    f = uniform_zero_mean(c.ndofs, 0)
+    u = uniform_vector(c.ndofs, 1)
+    ug = _t(u)
+    g.schwarz_smooth(ug, _t(f), steps=1)
+    assert _rel(_n(ug), H.smooth(H.L, u, f, 1)) <= TOL
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    g.pmg_vcycle(ug, _t(f))
+    assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f)) <= TOL
