@@ -36,8 +36,9 @@ enum { PMG_OK = 0, PMG_EINVAL = 1, PMG_EDIM = 2, PMG_ESINGULAR = 3, PMG_ECUDA = 
 
 /* dg_setup — discretisation of -lap u = f on the periodic box [0,lx]x[0,ly]x[0,lz]
  * (Eq. 1) with nx*ny*nz Cartesian elements of degree P on GL or GLL nodes
- * (Eqs. 2-6), SIPG penalty mu_d = penalty * P_l(P_l+1)/Delta_d per level and
- * direction (the paper uses penalty = 2).  Builds the p-multigrid hierarchy
+ * (Eqs. 2-6), SIPG penalty mu_d = penalty * mu_thr with mu_thr = P_l(P_l+1)/(2 Delta_d)
+ * the coercivity threshold of this SIPG form, per level and direction ("mu_min is
+ * the stability threshold"; the paper uses penalty = 2; reading R2).  Builds the p-multigrid hierarchy
  * P_l = 2^l, l = 0..L.  Host-only (no GPU needed).
  * Errors: PMG_EINVAL if P < 2 or P not a power of two or P > 32, any n_i < 3, l_i <= 0,
  *         penalty <= 0, basis not GLL/GL.  *out is set to NULL on error. */

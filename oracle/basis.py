@@ -103,5 +103,14 @@ def face_distances(basis, P):
 
 
 def penalty_min(P, delta):
-    """mu_min = P(P+1)/Delta (PAPER.md:331-334)."""
+    """The printed example mu_min = P(P+1)/Delta."""
     return P * (P + 1) / delta
+
+
+def stability_threshold(P, delta):
+    """Coercivity threshold of this SIPG normalisation (reading R2): the smallest mu for
+    which the periodic 1D IP matrix is positive semi-definite is P(P+1)/(2 Delta) -- half the
+    printed example; PAPER.md:331-333 defines mu_min as "the stability threshold", so the paper's
+    mu = 2 mu_min is mu = 2 * stability_threshold.  Pinned by tests/test_oracle_operator.py
+    (bisection on the explicit 1D matrix) and by Table 1 rows 1 and 7 (profiles/)."""
+    return P * (P + 1) / (2.0 * delta)

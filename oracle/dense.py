@@ -7,7 +7,8 @@ O2  Global matrix A (PAPER.md:111-126 Eq. 4, :143-148 Eq. 6) assembled from the
         a(u,v) = sum_e int_e grad u . grad v
                - sum_F int_F ( {d_n u}[v] + {d_n v}[u] ) + sum_F int_F mu [u][v]
     [v] = v^- - v^+ across a face with normal n^- pointing from "-" to "+",
-    {w} = (w^- + w^+)/2, mu = penalty * P(P+1)/Delta_normal (PAPER.md:331-334).
+    {w} = (w^- + w^+)/2, mu = penalty * P(P+1)/(2 Delta_normal): penalty times the
+    stability threshold (reading R2).
     Volume: tensor GL/GLL quadrature at the (P+1)^3 collocation points;
     faces: tensor product of the two in-face 1D rules.  Periodic wrap.
 O7  Subdomain solve: A_ss = A[I_s, I_s] (R_s A R_s^T literally, PAPER.md:204-213
@@ -23,7 +24,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 import scipy.linalg as sla
 
-from .basis import basis_data, penalty_min
+from .basis import basis_data, stability_threshold
 from .overlap import resolve_overlap, window_1d, weights_1d
 from . import mg
 
@@ -72,7 +73,7 @@ def assemble_A(ne, length, P, basis, penalty):
         wface = wline * (delta[other[0]] / 2.0) * (delta[other[1]] / 2.0)
         off = [0, 0, 0]; off[d] = 1
         e_plus = elem_index(ne, ex + off[0], ey + off[1], ez + off[2])
-        mu = penalty * penalty_min(P, delta[d])
+        mu = penalty * stability_threshold(P, delta[d])
         s = 2.0 / delta[d]
         Jv = np.concatenate([bd["phi_p"], -bd["phi_m"]])              # [u] = u^- - u^+
         Gv = 0.5 * s * np.concatenate([bd["dphi_p"], bd["dphi_m"]])   # {d_n u}

@@ -24,7 +24,7 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
-from .basis import basis_data, penalty_min
+from .basis import basis_data, stability_threshold
 from .overlap import resolve_overlap, weights_1d
 from . import mg
 
@@ -37,7 +37,7 @@ def assemble_1d(basis, P, ne, delta, penalty):
     L = np.zeros((N, N))
     s = 2.0 / delta
     Kv = s * bd["D"].T @ np.diag(bd["w"]) @ bd["D"]
-    mu = penalty * penalty_min(P, delta)
+    mu = penalty * stability_threshold(P, delta)
     for e in range(ne):
         L[e * n:(e + 1) * n, e * n:(e + 1) * n] += Kv
     Jv = np.concatenate([bd["phi_p"], -bd["phi_m"]])

@@ -138,7 +138,9 @@ Op1D assemble_1d(const Basis1D &b, int ne, ld delta, ld penalty_factor) {
   Op1D op;
   const int n = b.n, N = ne * n;
   op.n = n; op.ne = ne; op.delta = delta;
-  op.mu = penalty_factor * ld(b.P) * (b.P + 1) / delta;
+  // mu = penalty * mu_thr, mu_thr = P(P+1)/(2 Delta) the coercivity threshold of this SIPG
+  // normalisation ("mu_min is the stability threshold"; R2)
+  op.mu = penalty_factor * ld(b.P) * (b.P + 1) / (2 * delta);
   const ld s = 2 / delta;
   op.Dblk.assign(n * n, 0);
   for (int i = 0; i < n; ++i)

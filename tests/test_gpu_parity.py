@@ -265,3 +265,45 @@ def test_large_windows_global_path(c):
     ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
     g.pmg_vcycle(ug, _t(f))
     assert _rel(_n(ug), mg.vcycle(H, np.zeros_like(f), f)) <= TOL
+
+
+def _table1():
+    import os
+    rows = {}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "table1_rates.txt")):
+        line = line.split("#")[0].split()
+        if line:
+            rows[int(line[0])] = (line[1], line[2], OverlapSpec(int(line[3]), float(line[4]), int(line[5])),
+                                  [float(x) for x in line[6:10]])
+    return rows
+
+
+@pytest.mark.parametrize("row,P", [(1, 16), (1, 32), (7, 16), (7, 32), (2, 32), (8, 32)])
+def test_table1_rates_at_paper_scale(row, P):
+    """The GPU (parity-pinned to the oracle) reproduces Table 1 at the paper's own grids for the
+    one-node-overlap rows (which do not depend on the unpinned hat-weight quintic, reading R6):
+    -lg rho within 0.06 of the printed value (paper protocol: random guess in [-1,1], RHS
+    M 3 sin x sin y sin z, iterate to 1e-10)."""
+    import math
+    basis, solver, ov, paper = _table1()[row]
+    from paper_1612_04796_b200 import DG
+    ne = 128 // P
+    L2 = 2 * math.pi
+    g = DG((ne, ne, ne), (L2, L2, L2), P, 0 if basis == "GLL" else 1, 2.0, ov)
+    f = g.rhs_sin(3.0, 1.0, 1.0, 1.0)
+    u = _t(uniform_vector(g.ndofs(), 3))
+    if solver == "MG-CG":
+        _, hist, ok = g.pcg_solve(u, f, rtol=1e-10, maxit=80)
+        assert ok
+    else:
+        r = g.residual(u, f)
+        hist = [math.sqrt(g.dot(r, r))]
+        for _ in range(80):
+            g.pmg_vcycle(u, f)
+            r = g.residual(u, f)
+            hist.append(math.sqrt(g.dot(r, r)))
+            if hist[-1] <= 1e-10 * hist[0]:
+                break
+    lg = -math.log10((hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)))
+    want = paper[[4, 8, 16, 32].index(P)]
+    assert abs(lg - want) <= 0.06, (lg, want)

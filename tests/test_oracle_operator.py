@@ -97,3 +97,24 @@ def test_convergence_order(basis, P):
     # observed order between 6^3 and 12^3; theory h^{P+1} (GLL odd P superconverges nodally)
     order = np.log2(_solve_manufactured((6, 6, 6), P, basis) / _solve_manufactured((12, 12, 12), P, basis))
     assert P + 0.75 <= order <= P + 2.25, order
+
+
+@pytest.mark.parametrize("basis", [GLL, GL])
+@pytest.mark.parametrize("P", [1, 2, 4, 8, 16])
+def test_stability_threshold(basis, P):
+    """Reading R2: the coercivity threshold of the 1D SIPG matrix is P(P+1)/(2 Delta) exactly
+    (PSD just above, indefinite just below) -- PAPER.md:331-333 defines mu_min as that threshold."""
+    from oracle.basis import stability_threshold
+    delta = 0.37
+    thr = stability_threshold(P, delta)
+    for fac, psd in ((1.0 + 1e-6, True), (1.0 - 1e-3, False)):
+        mu_factor = fac            # penalty factor multiplies the threshold
+        L, _ = assemble_1d(basis, P, 6, delta, mu_factor)   # even n_e: the alternating mode exists
+        ev = np.linalg.eigvalsh(0.5 * (L + L.T))
+        tol = 1e-10 * np.max(np.abs(ev))
+        assert (ev[0] >= -tol) == psd, (fac, ev[:2])
+    # penalty factor 2 (the paper's mu = 2 mu_min): one-dimensional null space, rest positive
+    L, _ = assemble_1d(basis, P, 5, delta, 2.0)
+    ev = np.linalg.eigvalsh(0.5 * (L + L.T))
+    assert abs(ev[0]) < 1e-10 * ev[-1] and ev[1] > 1e-8 * ev[-1]
+    assert thr == P * (P + 1) / (2 * delta)
