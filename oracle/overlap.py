@@ -9,9 +9,11 @@ Readings (R5-R7):
   units, element width 2) satisfies d <= delta_ref (GLL) or d < delta_ref (GL),
   tolerance 1e-12, delta_ref = 2 delta_O / Delta_d; then max with the floor and
   cap at n = P+1.  FixedNodes(n_o) -> min(n_o, n).
-* delta_ref used by the weight: Relative/MaxRelative -> the geometric 2 delta_O/Delta;
-  FixedNodes(n_o), or a count raised by the floor -> midpoint between the n_o-th
-  and (n_o+1)-th neighbour node distance (2 if n_o = n).
+* Reach of the weight transition (reading R6): the "subdomain boundary" of the Fig. 2 caption is
+  the first neighbour node OUTSIDE the window (where the subdomain problem is Dirichlet-
+  truncated): delta_ref = d_{n_o+1}, or 2 if the window covers the whole neighbour; this one
+  rule serves every overlap mode.  It reproduces Table 1 rows 3, 4, 9, 13 (GPU sweep in
+  profiles/), where the geometric reach 2 delta_O / Delta did not.
 * Hat weight (Fig. 2 caption): xi_H = xi in the own element,
   xi -/+ 2 in the left/right neighbour; h = min(delta_ref, 1) (0 if the side has
   no overlap layer); t = (1 + h - |xi_H|) / (2 h) clipped to [0, 1];
@@ -34,14 +36,10 @@ def _count(basis, P, delta_ref):
     return int(np.sum(d < delta_ref - TOL))
 
 
-def _midpoint(basis, P, n_o):
+def _first_excluded(basis, P, n_o):
+    """Face distance of the first neighbour node outside the window (2: whole neighbour inside)."""
     d = face_distances(basis, P)
-    n = P + 1
-    if n_o >= n:
-        return 2.0
-    if n_o == 0:
-        return 0.0
-    return 0.5 * (d[n_o - 1] + d[n_o])
+    return 2.0 if n_o >= P + 1 else float(d[n_o])
 
 
 def resolve_overlap(mode, value, floor, basis, P, deltas):
@@ -53,7 +51,7 @@ def resolve_overlap(mode, value, floor, basis, P, deltas):
         if mode == OVL_NODES:
             n_o = min(int(value), n)
             n_o2 = min(max(n_o, floor), n)
-            out.append((n_o2, _midpoint(basis, P, n_o2)))
+            out.append((n_o2, _first_excluded(basis, P, n_o2)))
             continue
         if mode == OVL_REL:
             delta_O = value * dd
@@ -61,12 +59,9 @@ def resolve_overlap(mode, value, floor, basis, P, deltas):
             delta_O = min(value * dmax, dd)
         else:
             raise ValueError("unknown overlap mode")
-        dref = 2.0 * delta_O / dd
-        c = min(_count(basis, P, dref), n)
-        if floor > c:
-            c = min(floor, n)
-            dref = _midpoint(basis, P, c)
-        out.append((c, dref))
+        c = min(_count(basis, P, 2.0 * delta_O / dd), n)
+        c = min(max(c, floor), n)
+        out.append((c, _first_excluded(basis, P, c)))
     return out
 
 

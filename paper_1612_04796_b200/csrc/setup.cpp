@@ -212,28 +212,25 @@ Overlap1D resolve_overlap(int mode, double value, int floor_layers, const Basis1
   const ld tol = 1e-12L;
   std::vector<ld> d(n);
   for (int i = 0; i < n; ++i) d[i] = b.x[i] + 1;         // distance from the face, ref. units
-  auto midpoint = [&](int no) -> ld {
-    if (no >= n) return 2;
-    if (no <= 0) return 0;
-    return (d[no - 1] + d[no]) / 2;
-  };
   Overlap1D ov;
+  // Hat-weight reach (reading R6): the transition runs from 0 at the subdomain boundary -- the
+  // first neighbour node OUTSIDE the window, where the subdomain problem is Dirichlet-truncated
+  // -- to 1 at the mirror point inside the core: dref = d_{n_o+1} (2 if the window covers the
+  // whole neighbour); the weight uses h = min(dref, 1).
+  auto first_excluded = [&](int no) -> ld { return no < n ? d[no] : ld(2); };
   if (mode == 0) {
     ov.no = std::min(std::max((int)value, floor_layers), n);
-    ov.dref = midpoint(ov.no);
+    ov.dref = first_excluded(ov.no);
     return ov;
   }
   ld deltaO = (mode == 1) ? ld(value) * delta_d : std::min(ld(value) * delta_max, delta_d);
-  ld dref = 2 * deltaO / delta_d;
+  const ld dref = 2 * deltaO / delta_d;       // overlap width in reference units
   int c = 0;
   for (int i = 0; i < n; ++i)
     if (b.kind == 0 ? (d[i] <= dref + tol) : (d[i] < dref - tol)) ++c;
   c = std::min(c, n);
-  if (floor_layers > c) {
-    c = std::min(floor_layers, n);
-    dref = midpoint(c);
-  }
-  ov.no = c; ov.dref = dref;
+  if (floor_layers > c) c = std::min(floor_layers, n);
+  ov.no = c; ov.dref = first_excluded(c);
   return ov;
 }
 
