@@ -224,7 +224,11 @@ struct LineSpec {
   const double *Ext; int next, esr, esp, esq;
 };
 
-template <int DIR, int KS, int MT, class Epi>
+// TAIL: the output extent is 8*MT + 1 (n = 2^l + 1 everywhere in this method); rows [0, 8 MT)
+// go through DMMA and the last row through FP64 FMAs on the B fragments already in registers
+// (each lane sums its k's, then a 2-step shuffle over the 4 lanes that share a column), which
+// avoids padding 17 -> 24 (or 9 -> 16) rows on the tensor path.
+template <int DIR, int KS, int MT, bool TAIL, class Epi>
 __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const LineSpec &ls,
                                             Epi &epi) {
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
@@ -243,6 +247,14 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
       const int o = mt * 8 + g, k = ks * 4 + t;
       a[mt][ks] = (o < mo && k < kt) ? ls.Amat[o * ls.ao + k * ls.ak] : 0.0;
     }
+  double at[TAIL ? KS : 1];
+  if (TAIL) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + t;
+      at[ks] = k < kt ? ls.Amat[(8 * MT) * ls.ao + k * ls.ak] : 0.0;
+    }
+  }
   int koff[KS];
   bool kext[KS];
 #pragma unroll
@@ -254,10 +266,12 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
   const int ntiles = (ncol + 7) >> 3;
   for (int tile = 2 * warp; tile < ntiles; tile += 2 * nw) {
     double b[2][KS];
+    int pbq[2], qbq[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int nb = min(min(tile + u, ntiles - 1) * 8 + g, ncol - 1);
       const int q = __umulhi((unsigned)nb, magic), p = nb - q * mp;
+      pbq[u] = p; qbq[u] = q;
       const double *xb = X + p * sp + q * sq;
       const double *eb = ls.Ext ? ls.Ext + p * ls.esp + q * ls.esq : X;
 #pragma unroll
@@ -274,6 +288,16 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) dmma884(c[u][mt][0], c[u][mt][1], a[mt][ks], b[u][ks]);
+    double tl[2] = {0.0, 0.0};
+    if (TAIL) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) tl[u] = fma(at[ks], b[u][ks], tl[u]);
+        tl[u] += __shfl_xor_sync(0xffffffffu, tl[u], 1);
+        tl[u] += __shfl_xor_sync(0xffffffffu, tl[u], 2);
+      }
+    }
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -290,6 +314,10 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
           if (o < mo) epi.template put<DIR>(o, p, q, cf, c[u][mt][j]);
         }
       }
+      if (TAIL && t == 0 && (tile + u) * 8 + g < ncol) {
+        const double cf = epi.template col<DIR>(pbq[u], qbq[u]);
+        epi.template put<DIR>(8 * MT, pbq[u], qbq[u], cf, tl[u]);
+      }
     }
   }
 }
@@ -299,8 +327,16 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
 template <int DIR, int KSMAX, class Epi>
 __device__ void mma_lines_gen(const double *X, const Blk &B, const LineSpec &ls, Epi &epi) {
   const int KS = (ls.mk + ls.next + 3) >> 2, MT = (ls.mo + 7) >> 3;
+  if (ls.mo > 8 && (ls.mo & 7) == 1) {           // 8k+1 rows: DMMA for 8k, FMA tail row
+    const int MTT = ls.mo >> 3;
+#define PMG_TTILE(ks, mt) \
+    if (ks <= KSMAX && KS <= ks && MTT == mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt, true>(X, B, ls, epi); return; }
+    PMG_TTILE(2, 1) PMG_TTILE(3, 1) PMG_TTILE(4, 1) PMG_TTILE(5, 1) PMG_TTILE(3, 2) PMG_TTILE(5, 2)
+    PMG_TTILE(6, 2)
+#undef PMG_TTILE
+  }
 #define PMG_TILE(ks, mt) \
-  if (ks <= KSMAX && KS <= ks && MT <= mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt>(X, B, ls, epi); return; }
+  if (ks <= KSMAX && KS <= ks && MT <= mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt, false>(X, B, ls, epi); return; }
   PMG_TILE(1, 1) PMG_TILE(2, 1) PMG_TILE(2, 2) PMG_TILE(3, 1) PMG_TILE(3, 2) PMG_TILE(3, 3)
   PMG_TILE(4, 2) PMG_TILE(5, 2) PMG_TILE(5, 3) PMG_TILE(6, 3) PMG_TILE(7, 4) PMG_TILE(8, 4)
 #undef PMG_TILE
