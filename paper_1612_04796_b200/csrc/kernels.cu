@@ -553,7 +553,7 @@ __device__ __forceinline__ void fdm_phases(double *X, const int *m, double *cons
 
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
 template <int KSMAX>
-__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
                                                  double *__restrict__ Z) {
   extern __shared__ double sm[];
   const int n = L.n, n3 = n * n * n;
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_fdm_mma(LevelDev L,
 // c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
 // c1 = -tdR/2 - mu tvR, c2 = tvR/2, c3 = tdL/2 - mu tvL, c4 = -tvL/2.
 template <int KSMAX>
-__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
                                                       const double *__restrict__ T,
                                                       const double *__restrict__ f,
                                                       double *__restrict__ out,
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_apply_mma(LevelDev 
 // memory, u_f written back, and the traces of the new u_f emitted for the residual.
 // smem: Uc (nc^3) | T1 (nf nc^2) | T2 (nf^2 nc) | U (nf^3) | trs (12 nf)
 template <int KSMAX>
-__global__ void __launch_bounds__(256, KSMAX <= 4 ? 4 : 2) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
                                                         const double *__restrict__ uc,
                                                         double *__restrict__ uf,
                                                         double *__restrict__ T) {
@@ -1468,8 +1468,9 @@ cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, c
                                   double *uf, double *T, cudaStream_t s) {
   configure_smem();
   const size_t sb = prolong_traces_smem(Lf.n, nc);
-  if (((nc + 3) >> 2) <= 2) k_prolong_traces<2><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
-  else if (((nc + 3) >> 2) <= 4) k_prolong_traces<4><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
+  if (Lf.n >= 17) k_prolong_traces<8><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);   // big blocks: 8 warps
+  else if (((nc + 3) >> 2) <= 2) k_prolong_traces<2><<<Lf.Ne, 128, sb, s>>>(Lf, nc, I, uc, uf, T);
+  else if (((nc + 3) >> 2) <= 4) k_prolong_traces<4><<<Lf.Ne, 128, sb, s>>>(Lf, nc, I, uc, uf, T);
   else k_prolong_traces<8><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
   return cudaGetLastError();
 }
@@ -1484,8 +1485,8 @@ cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *
   configure_smem();
   const size_t sb = apply_mma_smem(L.n);
   const int ks = (L.n + 4 + 3) >> 2;
-  if (ks <= 2) k_apply_mma<2><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
-  else if (ks <= 4) k_apply_mma<4><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  if (ks <= 2) k_apply_mma<2><<<L.Ne, 128, sb, s>>>(L, u, T, f, out, I, nc, fc);
+  else if (ks <= 4) k_apply_mma<4><<<L.Ne, 128, sb, s>>>(L, u, T, f, out, I, nc, fc);
   else k_apply_mma<8><<<L.Ne, 256, sb, s>>>(L, u, T, f, out, I, nc, fc);
   return cudaGetLastError();
 }
@@ -1517,8 +1518,8 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
     configure_smem();
     const size_t sb = fdm_mma_smem_bytes(L);
     const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
-    if (ks <= 2) k_fdm_mma<2><<<L.Ne, 256, sb, s>>>(L, r, Z);
-    else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 256, sb, s>>>(L, r, Z);
+    if (ks <= 2) k_fdm_mma<2><<<L.Ne, 128, sb, s>>>(L, r, Z);
+    else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 128, sb, s>>>(L, r, Z);
     else k_fdm_mma<8><<<L.Ne, 256, sb, s>>>(L, r, Z);
     return cudaGetLastError();
   }
