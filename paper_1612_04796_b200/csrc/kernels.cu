@@ -1037,9 +1037,11 @@ __global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restr
 // Register-only fold: one thread per DOF issues all (up to 27) predicated loads of the
 // weighted window values that cover it before summing them in a fixed order -> maximal
 // memory-level parallelism, deterministic result.  NT = compile-time n (fast index math).
-template <int NT>
+template <int NT, bool TR>
 __global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restrict__ Z,
-                                               double *__restrict__ u, int zero) {
+                                               double *__restrict__ u, int zero,
+                                               double *__restrict__ T) {
+  extern __shared__ double sm[];          // TR: the folded element (n^3) + trace table (12 n)
   const int n = NT > 0 ? NT : L.n;
   const int n3 = n * n * n;
   const int mx = L.m[0], my = L.m[1];
@@ -1084,6 +1086,34 @@ __global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restr
       for (int q = 0; q < 9; ++q) du += z[q];
     }
     u[g] = du;
+    if (TR) sm[t] = du;
+  }
+  if (!TR) return;
+  // fused trace pass of the following residual: face values / derivatives of the new u
+  const int n2 = n * n;
+  double *trs = sm + n3;
+  for (int d = 0; d < 3; ++d)
+    for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) trs[d * 4 * n + i] = L.tr[d][i];
+  __syncthreads();
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = sm[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
   }
 }
 
@@ -1538,16 +1568,34 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
 cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
                         cudaStream_t s) {
   const int z = zero ? 1 : 0;
-  switch (L.n) {
-    case 3: k_fold2<3><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
-    case 5: k_fold2<5><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
-    case 9: k_fold2<9><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
-    case 17: k_fold2<17><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
-    case 33: k_fold2<33><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
-    default: k_fold2<0><<<L.Ne, 256, 0, s>>>(L, Z, u, z); break;
+  const size_t sb = T ? sizeof(double) * ((size_t)L.n * L.n * L.n + 12 * L.n) : 0;
+  if (T && sb > 48 * 1024) {
+    static bool cfg = false;
+    if (!cfg) {
+      cfg = true;
+      cudaFuncSetAttribute(k_fold2<17, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_fold2<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
   }
+#define PMG_FOLD(NN)                                                                          \
+  if (T) k_fold2<NN, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);                             \
+  else k_fold2<NN, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+  if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
+    k_fold2<33, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    cudaError_t e0 = cudaGetLastError();
+    if (e0 == cudaSuccess) e0 = launch_traces(L, u, T, s);
+    return e0;
+  }
+  switch (L.n) {
+    case 3: PMG_FOLD(3) break;
+    case 5: PMG_FOLD(5) break;
+    case 9: PMG_FOLD(9) break;
+    case 17: PMG_FOLD(17) break;
+    case 33: PMG_FOLD(33) break;
+    default: PMG_FOLD(0) break;
+  }
+#undef PMG_FOLD
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && T) e = launch_traces(L, u, T, s);
   return e;
 }
 static size_t xfer_smem(int nf, int nc) {
