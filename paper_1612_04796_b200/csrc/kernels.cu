@@ -1581,7 +1581,10 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
   if (T) k_fold2<NN, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);                             \
   else k_fold2<NN, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
   if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
-    k_fold2<33, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    if (L.n == 33) k_fold2<33, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else if (L.n == 5) k_fold2<5, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else if (L.n == 3) k_fold2<3, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else k_fold2<0, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
     cudaError_t e0 = cudaGetLastError();
     if (e0 == cudaSuccess) e0 = launch_traces(L, u, T, s);
     return e0;
