@@ -11,6 +11,10 @@
 
 namespace pmg {
 
+#ifndef FDM_BIG_THREADS
+#define FDM_BIG_THREADS 256
+#endif
+
 namespace {
 
 __device__ __forceinline__ int wrap(int a, int n) { return a < 0 ? a + n : (a >= n ? a - n : a); }
@@ -204,9 +208,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
+  r = fma(r, e, r);               // ~2^-46 relative
   e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  return fma(r, e, r);            // full precision (keeps the 1e-11 parity margin untouched)
 }
 
 template <int DIR> struct Other {
@@ -518,8 +522,22 @@ __device__ __forceinline__ void fdm_offsets(const LevelDev &L, int e, long long 
 
 __device__ __forceinline__ void fdm_gather(const LevelDev &L, const double *r, const long long *offs,
                                            double *X) {
-  const int m0 = L.m[0], m1 = L.m[1];
+  const int m0 = L.m[0], m1 = L.m[1], m2 = L.m[2];
   const long long *xo = offs, *yo = offs + m0, *zo = offs + m0 + m1;
+  if (m0 <= 32) {
+    // one warp per window row (b, c), lane = a: the row base is warp-uniform, xo[a] per lane
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long xa = lane < m0 ? xo[lane] : 0;
+    const int rows = m1 * m2;
+    int b = warp % m1, c = warp / m1;
+    const int db = nw % m1, dc = nw / m1;
+    for (int row = warp; row < rows; row += nw) {
+      if (lane < m0) cp_async8(X + lane + m0 * row, r + xa + yo[b] + zo[c]);
+      b += db; c += dc;
+      if (b >= m1) { b -= m1; ++c; }
+    }
+    return;
+  }
   const int total = L.Mw;
   int a = threadIdx.x % m0, bc = threadIdx.x / m0;
   int b = bc % m1, c = bc / m1;
@@ -553,78 +571,33 @@ __device__ __forceinline__ void fdm_phases(double *X, const int *m, double *cons
 
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
 template <int KSMAX>
-__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : FDM_BIG_THREADS, KSMAX <= 4 ? 8 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
                                                  double *__restrict__ Z) {
   extern __shared__ double sm[];
-  const int n = L.n, n3 = n * n * n;
   const int m[3] = {L.m[0], L.m[1], L.m[2]};
   const int Mw = L.Mw;
   double *X = sm;
   double *Ss[3];
   double *lam[3], *W[3];
-  {
-    double *p = sm + Mw;
-    for (int d = 0; d < 3; ++d) { Ss[d] = p; p += m[d] * m[d]; }
-    for (int d = 0; d < 3; ++d) { lam[d] = p; p += m[d]; }
-    for (int d = 0; d < 3; ++d) { W[d] = p; p += m[d]; }
-  }
+  double *p = sm + Mw;
+  for (int d = 0; d < 3; ++d) { Ss[d] = p; p += m[d] * m[d]; }
+  for (int d = 0; d < 3; ++d) { lam[d] = p; p += m[d]; }
+  for (int d = 0; d < 3; ++d) { W[d] = p; p += m[d]; }
+  long long *offs = reinterpret_cast<long long *>(p);
   for (int d = 0; d < 3; ++d) {
     stage(Ss[d], L.S[d], m[d] * m[d]);
     stage(lam[d], L.lam[d], m[d]);
     stage(W[d], L.W[d], m[d]);
   }
   const int e = blockIdx.x;
-  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  // gather offsets: global address of window node (a, b, c) = xoff[a] + yoff[b] + zoff[c]
-  long long *offs = reinterpret_cast<long long *>(W[2] + m[2]);
-  {
-    const long long estride[3] = {(long long)n3, (long long)L.nx * n3, (long long)L.nx * L.ny * n3};
-    const int lstride[3] = {1, n, n * n};
-    int base = 0;
-    for (int d = 0; d < 3; ++d) {
-      const int no = L.no[d];
-      for (int a = threadIdx.x; a < m[d]; a += blockDim.x) {
-        const int o = a < no ? -1 : (a < no + n ? 0 : 1);
-        const int li = a < no ? n - no + a : (a < no + n ? a - no : a - no - n);
-        offs[base + a] = wrap(ec[d] + o, edim[d]) * estride[d] + li * lstride[d];
-      }
-      base += m[d];
-    }
-  }
+  fdm_offsets(L, e, offs);
   __syncthreads();
-  {
-    const long long *xo = offs, *yo = offs + m[0], *zo = offs + m[0] + m[1];
-    const int total = m[0] * m[1] * m[2];
-    // thread-linear over the window: coalesced-ish global reads, contiguous smem writes
-    int a = threadIdx.x % m[0], bc = threadIdx.x / m[0];
-    int b = bc % m[1], c = bc / m[1];
-    const int da = blockDim.x % m[0], dbc = blockDim.x / m[0];
-    for (int w = threadIdx.x; w < total; w += blockDim.x) {
-      cp_async8(X + w, r + xo[a] + yo[b] + zo[c]);
-      a += da; b += dbc;
-      if (a >= m[0]) { a -= m[0]; ++b; }
-      while (b >= m[1]) { b -= m[1]; ++c; }
-    }
-  }
+  fdm_gather(L, r, offs, X);
   cp_async_wait_all();
   __syncthreads();
-  const Blk B = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};
-  EpiStore st{X, B};
-  EpiDivide dv{X, B, {lam[0], lam[1], lam[2]}};
-  EpiWeightStore ws{Z + (long long)e * Mw, B, {W[0], W[1], W[2]}};
-  // forward: A = S^T, i.e. A[o][k] = S[k*m + o]
-  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], 1, m[0], st); __syncthreads();
-  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], 1, m[1], st); __syncthreads();
   const double *lamc[3] = {lam[0], lam[1], lam[2]};
-  if (!fdm_z_fused<KSMAX>(X, B, Ss[2], lamc)) {
-    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], 1, m[2], dv); __syncthreads();
-    // backward: A = S
-    mma_lines_dispatch<2, KSMAX>(X, B, Ss[2], m[2], 1, st);
-  }
-  __syncthreads();
-  mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], m[1], 1, st); __syncthreads();
-  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
+  const double *Wc[3] = {W[0], W[1], W[2]};
+  fdm_phases<KSMAX>(X, m, Ss, lamc, Wc, Z + (long long)e * Mw);
 }
 
 // smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
@@ -1550,7 +1523,7 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
     const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
     if (ks <= 2) k_fdm_mma<2><<<L.Ne, 128, sb, s>>>(L, r, Z);
     else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 128, sb, s>>>(L, r, Z);
-    else k_fdm_mma<8><<<L.Ne, 256, sb, s>>>(L, r, Z);
+    else k_fdm_mma<8><<<L.Ne, FDM_BIG_THREADS, sb, s>>>(L, r, Z);
     return cudaGetLastError();
   }
   if (smem) {
