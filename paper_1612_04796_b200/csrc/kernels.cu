@@ -398,18 +398,6 @@ struct EpiAcc {
     else V[w] += v;
   }
 };
-// mass-weighted accumulation of one term of Eq. 7 into V
-struct EpiMassAcc {
-  double *V; Blk B; const double *mass[3]; bool first;
-  template <int DIR> __device__ __forceinline__ double col(int p, int q) const {
-    return mass[Other<DIR>::P][p] * mass[Other<DIR>::Q][q];
-  }
-  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
-    const int w = blk_index<DIR>(B, o, p, q);
-    if (first) V[w] = cf * v;
-    else V[w] += cf * v;
-  }
-};
 
 // Fused z passes of the fast diagonalisation: forward S_z^T, eigen-divide, backward S_z on the
 // same z columns.  A warp owns its columns through both GEMMs, so no block barrier is needed
@@ -965,45 +953,6 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
     }
     double *Td = Te + d * 4 * n2;
     Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
-}
-
-// Deterministic weighted scatter-add (Eq. 10): every DOF pulls the weighted corrections of
-// the (<= 3 per direction) subdomains whose window contains it, in a fixed order; u += du.
-__global__ void k_fold(LevelDev L, const double *__restrict__ Z, double *__restrict__ u,
-                       int zero) {
-  const int n = L.n, n3 = n * n * n;
-  const int mx = L.m[0], my = L.m[1], Mw = L.Mw;
-  const int e = blockIdx.x;
-  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
-    const int idx[3] = {t % n, (t / n) % n, t / (n * n)};
-    int cnt[3], off[3][3], wi[3][3];
-    for (int d = 0; d < 3; ++d) {
-      const int no = L.no[d], i = idx[d];
-      int c = 0;
-      // subdomain centred on the left neighbour: this node is in its right overlap
-      if (i < no) { off[d][c] = -1; wi[d][c] = no + n + i; ++c; }
-      off[d][c] = 0; wi[d][c] = no + i; ++c;
-      // subdomain centred on the right neighbour: this node is in its left overlap
-      if (i >= n - no) { off[d][c] = 1; wi[d][c] = i - (n - no); ++c; }
-      cnt[d] = c;
-    }
-    double du = 0;
-    for (int cz = 0; cz < cnt[2]; ++cz) {
-      const int sz = wrap(ec[2] + off[2][cz], edim[2]);
-      for (int cy = 0; cy < cnt[1]; ++cy) {
-        const int sy = wrap(ec[1] + off[1][cy], edim[1]);
-        for (int cx = 0; cx < cnt[0]; ++cx) {
-          const int sx = wrap(ec[0] + off[0][cx], edim[0]);
-          const long long s = sx + L.nx * (sy + (long long)L.ny * sz);
-          du += __ldg(Z + s * Mw + wi[0][cx] + mx * (wi[1][cy] + my * wi[2][cz]));
-        }
-      }
-    }
-    const long long g = (long long)e * n3 + t;
-    u[g] = zero ? du : u[g] + du;
   }
 }
 
