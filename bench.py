@@ -28,7 +28,7 @@ FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 TF: 64 DFMA/clk/SM 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
@@ -264,6 +264,12 @@ def run_ours(args, rank, world, local_rank):
                               "ms_per_cycle": round(v[0] / max(pcycles, 1), 4)}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     cyc_t_roof = max(flops / (peak_tf * 1e12), bytes_ / 6554.6e9)
+    traffic = None      # DRAM bytes per launch of the roofline kernel from the committed ncu capture
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(args.config, {}).get("k_fdm_mma_top")
+    except Exception:
+        pass
     out = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -281,7 +287,8 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 8 * N},
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": None,
+                     "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": traffic,
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
                      "kernel": "k_fdm_mma (Schwarz fast-diagonalisation solve, top level)",
                      "kernel_ms_per_launch": fdm_avg_ms,
                      "share_of_step": (fdm_ms / args.steps / ms_profiled) if ms_profiled else None,

@@ -307,3 +307,32 @@ def test_table1_rates_at_paper_scale(row, P):
     lg = -math.log10((hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)))
     want = paper[[4, 8, 16, 32].index(P)]
     assert abs(lg - want) <= 0.06, (lg, want)
+
+
+def test_c2_manufactured_solution_accuracy():
+    """NEXT row f4 / BASELINE c2: V(1,1) cycles on the GPU until ||r||/||r0|| <= 1e-10 for
+    f = M 3 sin x sin y sin z; the discrete solution approximates u = sin x sin y sin z to
+    O(h^{P+1}) (P = 8, h = pi/4: nodal error well below 1e-6), and the per-cycle reduction is
+    the paper's row-13 regime (-lg rho = 1.75 at P = 8)."""
+    import math
+    from oracle.dense import node_coords
+    c = get_config("c2")
+    g = _gpu(c)
+    f = g.rhs_sin(3.0, 1.0, 1.0, 1.0)
+    u = torch.zeros_like(f)
+    r0 = math.sqrt(g.dot(f, f))
+    hist = [r0]
+    for _ in range(30):
+        g.pmg_vcycle(u, f)
+        r = g.residual(u, f)
+        hist.append(math.sqrt(g.dot(r, r)))
+        if hist[-1] <= 1e-10 * r0:
+            break
+    assert hist[-1] <= 1e-10 * r0
+    lg = -math.log10((hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)))
+    assert lg > 1.0, lg          # zero initial guess + smooth RHS on 8^3 (paper: 16^3, random guess)
+    X, Y, Z = node_coords(c.ne, c.length, c.P, c.basis)
+    ue = np.sin(X) * np.sin(Y) * np.sin(Z)
+    err = _n(u) - ue
+    err -= err.mean()
+    assert np.max(np.abs(err)) < 1e-6, np.max(np.abs(err))
