@@ -41,6 +41,7 @@ _sig = {
     "dg_launch_count": (_ll, [_vp]),
     "dg_profile": (_i, [_vp, _i]),
     "dg_set_graphs": (_i, [_vp, _i]),
+    "dg_set_colored": (_i, [_vp, _i]),
     "dg_profile_read": (_i, [_vp, _dp, C.POINTER(_ll), _i]),
     "pmg_fp64_peak": (_i, [_i, _dp, _vp]),
     "dg_last_error": (C.c_char_p, [_vp]),
@@ -118,6 +119,9 @@ class DG:
         return lib.dg_launch_count(self._c)
 
     PROF_KINDS = ("traces", "apply", "fdm", "fold", "restrict", "prolong", "coarse", "vec")
+
+    def set_colored(self, enable=True):
+        self._check(lib.dg_set_colored(self._c, 1 if enable else 0))
 
     def set_graphs(self, enable=True):
         self._check(lib.dg_set_graphs(self._c, 1 if enable else 0))

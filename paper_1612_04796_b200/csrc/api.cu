@@ -66,6 +66,7 @@ struct dg_ctx {
   std::string err;
   // CUDA-graph replay of whole V-cycles (dg_set_graphs); keyed by (u, f, zero_top)
   bool graphs = true;
+  bool colored = false;      // colored Schwarz scatter (dg_set_colored); measured slower on c3
   cudaStream_t cap_stream = nullptr;
   struct GraphEntry { double *u; const double *f; bool zero; cudaGraphExec_t exec; };
   std::vector<GraphEntry> graph_cache;
@@ -264,13 +265,21 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
       if (st) return st;
       rin = r;
     }
+    const bool emit = (it + 1 < steps) || traces_after;
+    if (h.fdm_path == 0 && c->colored && pmg::fdm_colored_ok(d)) {
+      // colored step: W du_s added straight into u, colour by colour (no Z round trip, no fold)
+      if (zero) LAUNCH(c, pmg::launch_zero(u, h.N, s));
+      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_colored(d, rin, u, s));
+      c->launches += 7;
+      if (emit) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
+      continue;
+    }
     if (h.fdm_path == 1) {
       LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_global(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
       c->launches += 6;
     } else {
       LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
     }
-    const bool emit = (it + 1 < steps) || traces_after;
     LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, emit ? T : nullptr, s));
   }
   if (steps == 0 && zero_init) LAUNCH(c, pmg::launch_zero(u, h.N, s));
@@ -743,6 +752,14 @@ int dg_rhs_sin(dg_ctx *c, double amp, double kx, double ky, double kz, double *b
 }
 
 long long dg_launch_count(const dg_ctx *c) { return c ? c->launches : -1; }
+
+int dg_set_colored(dg_ctx *c, int enable) {
+  if (!c) return PMG_EINVAL;
+  c->colored = enable != 0;
+  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
+  c->graph_cache.clear();
+  return PMG_OK;
+}
 
 int dg_set_graphs(dg_ctx *c, int enable) {
   if (!c) return PMG_EINVAL;

@@ -388,6 +388,18 @@ struct EpiWeightStore {
     Zg[blk_index<DIR>(G, o, p, q)] = v * (cf * W[DIR][o]);
   }
 };
+// weight and scatter-add straight into u (colored, race-free): window node (a,b,c) lives at
+// u[xo[a] + yo[b] + zo[c]]; fire-and-forget FP64 reductions (RED.ADD.F64) at L2
+struct EpiWeightRed {
+  double *u; const long long *offs; int m0, m1; const double *W[3];
+  template <int DIR> __device__ __forceinline__ double col(int p, int q) const {
+    return W[Other<DIR>::P][p] * W[Other<DIR>::Q][q];
+  }
+  template <int DIR> __device__ __forceinline__ void put(int o, int p, int q, double cf, double v) const {
+    static_assert(DIR == 0, "the scatter pass runs along x");
+    atomicAdd(u + offs[o] + offs[m0 + p] + offs[m0 + m1 + q], v * (cf * W[0][o]));
+  }
+};
 // plain accumulation into V (first pass stores)
 struct EpiAcc {
   double *V; Blk B; bool first;
@@ -541,11 +553,13 @@ __device__ __forceinline__ void fdm_gather(const LevelDev &L, const double *r, c
 template <int KSMAX>
 __device__ __forceinline__ void fdm_phases(double *X, const int *m, double *const *Ss,
                                            const double *const *lam, const double *const *W,
-                                           double *Ze) {
+                                           double *Ze, double *ured = nullptr,
+                                           const long long *offs = nullptr) {
   const Blk B = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};
   EpiStore st{X, B};
   EpiDivide dv{X, B, {lam[0], lam[1], lam[2]}};
   EpiWeightStore ws{Ze, B, {W[0], W[1], W[2]}};
+  EpiWeightRed wr{ured, offs, m[0], m[1], {W[0], W[1], W[2]}};
   mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], 1, m[0], st); __syncthreads();
   mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], 1, m[1], st); __syncthreads();
   if (!fdm_z_fused<KSMAX>(X, B, Ss[2], lam)) {
@@ -554,13 +568,15 @@ __device__ __forceinline__ void fdm_phases(double *X, const int *m, double *cons
   }
   __syncthreads();
   mma_lines_dispatch<1, KSMAX>(X, B, Ss[1], m[1], 1, st); __syncthreads();
-  mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
+  if (ured) mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, wr);
+  else mma_lines_dispatch<0, KSMAX>(X, B, Ss[0], m[0], 1, ws);
 }
 
 // Shared memory: window X (Mw) | S_x, S_y, S_z (m_d^2) | lam (3 m_d) | W (3 m_d)
 template <int KSMAX>
 __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : FDM_BIG_THREADS, KSMAX <= 4 ? 8 : 2) k_fdm_mma(LevelDev L, const double *__restrict__ r,
-                                                 double *__restrict__ Z) {
+                                                 double *__restrict__ Z, int color,
+                                                 double *__restrict__ u) {
   extern __shared__ double sm[];
   const int m[3] = {L.m[0], L.m[1], L.m[2]};
   const int Mw = L.Mw;
@@ -577,7 +593,12 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : FDM_BIG_THREADS, KSMAX <= 4
     stage(lam[d], L.lam[d], m[d]);
     stage(W[d], L.W[d], m[d]);
   }
-  const int e = blockIdx.x;
+  int e = blockIdx.x;
+  if (color >= 0) {       // subdomain bx of parity class `color` (2x2x2 colouring)
+    const int hx = L.nx >> 1, hy = L.ny >> 1;
+    const int bx = e % hx, by = (e / hx) % hy, bz = e / (hx * hy);
+    e = (2 * bx + (color & 1)) + L.nx * ((2 * by + ((color >> 1) & 1)) + L.ny * (2 * bz + (color >> 2)));
+  }
   fdm_offsets(L, e, offs);
   __syncthreads();
   fdm_gather(L, r, offs, X);
@@ -585,7 +606,7 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : FDM_BIG_THREADS, KSMAX <= 4
   __syncthreads();
   const double *lamc[3] = {lam[0], lam[1], lam[2]};
   const double *Wc[3] = {W[0], W[1], W[2]};
-  fdm_phases<KSMAX>(X, m, Ss, lamc, Wc, Z + (long long)e * Mw);
+  fdm_phases<KSMAX>(X, m, Ss, lamc, Wc, Z + (long long)e * Mw, color >= 0 ? u : nullptr, offs);
 }
 
 // smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
@@ -1464,15 +1485,36 @@ bool fdm_mma_ok(const LevelDev &L) {
   return L.m[0] <= 32 && L.m[1] <= 32 && L.m[2] <= 32 && fdm_mma_smem_bytes(L) <= 227 * 1024;
 }
 
+bool fdm_colored_ok(const LevelDev &L) {
+  if (!fdm_mma_ok(L)) return false;
+  if ((L.nx & 1) || (L.ny & 1) || (L.nz & 1)) return false;          // 2-colouring across the seam
+  for (int d = 0; d < 3; ++d)
+    if (2 * L.no[d] > L.n) return false;                            // same-colour windows disjoint
+  return true;
+}
+
+cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cudaStream_t s) {
+  configure_smem();
+  const size_t sb = fdm_mma_smem_bytes(L);
+  const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
+  const int grid = L.Ne / 8;
+  for (int color = 0; color < 8; ++color) {
+    if (ks <= 2) k_fdm_mma<2><<<grid, 128, sb, s>>>(L, r, nullptr, color, u);
+    else if (ks <= 4) k_fdm_mma<4><<<grid, 128, sb, s>>>(L, r, nullptr, color, u);
+    else k_fdm_mma<8><<<grid, FDM_BIG_THREADS, sb, s>>>(L, r, nullptr, color, u);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s) {
   if (fdm_mma_ok(L)) {
     configure_smem();
     const size_t sb = fdm_mma_smem_bytes(L);
     const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
-    if (ks <= 2) k_fdm_mma<2><<<L.Ne, 128, sb, s>>>(L, r, Z);
-    else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 128, sb, s>>>(L, r, Z);
-    else k_fdm_mma<8><<<L.Ne, FDM_BIG_THREADS, sb, s>>>(L, r, Z);
+    if (ks <= 2) k_fdm_mma<2><<<L.Ne, 128, sb, s>>>(L, r, Z, -1, nullptr);
+    else if (ks <= 4) k_fdm_mma<4><<<L.Ne, 128, sb, s>>>(L, r, Z, -1, nullptr);
+    else k_fdm_mma<8><<<L.Ne, FDM_BIG_THREADS, sb, s>>>(L, r, Z, -1, nullptr);
     return cudaGetLastError();
   }
   if (smem) {

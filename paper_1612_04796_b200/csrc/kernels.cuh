@@ -42,6 +42,11 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
 cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
                                 double *out, double *Cb, double *V, cudaStream_t s);
 bool fdm_mma_ok(const LevelDev &L);
+// Colored Schwarz step: 8 launches (parity classes of the element coordinates); same-colour
+// windows are node-disjoint, so each subdomain adds W du_s straight into u (no Z, no fold);
+// deterministic (fixed colour order).  Needs even n_e and 2 n_o <= n in every direction.
+bool fdm_colored_ok(const LevelDev &L);
+cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cudaStream_t s);
 // fused prolongation u_f += I u_c + traces of the new u_f (n_f <= 17)
 bool prolong_traces_ok(const LevelDev &Lf, int nc);
 cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, const double *uc,

@@ -336,3 +336,19 @@ def test_c2_manufactured_solution_accuracy():
     err = _n(u) - ue
     err -= err.mean()
     assert np.max(np.abs(err)) < 1e-6, np.max(np.abs(err))
+
+
+@pytest.mark.parametrize("name,ne", [("c1", None), ("c3", 4)])
+def test_colored_scatter_matches_oracle(name, ne):
+    """dg_set_colored(1): the Schwarz correction added colour by colour straight into u."""
+    c = get_config(name, ne)
+    g = _gpu(c)
+    g.set_colored(True)
+    H = _oracle(c)
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    u = np.zeros(c.ndofs)
+    for _ in range(2):
+        g.pmg_vcycle(ug, _t(f))
+        u = mg.vcycle(H, u, f)
+        assert _rel(_n(ug), u) <= TOL
