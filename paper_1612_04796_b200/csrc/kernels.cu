@@ -28,6 +28,30 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier (transaction bytes)
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned phase) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_addr(mbar)), "r"(phase) : "memory");
+}
+
 __device__ __forceinline__ void stage(double *dst, const double *src, int count) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) cp_async8(dst + i, src + i);
 }
@@ -622,23 +646,42 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_
                                                       int nc, double *__restrict__ fc) {
   extern __shared__ double sm[];
   const int n = L.n, n2 = n * n, n3 = n2 * n;
-  double *U = sm, *V = sm + n3, *Cf = sm + 2 * n3, *ms = Cf + 12 * n2;
+  // smem: U staging (n^3 + 2, 16-byte aligned superset of the element) | V | Cf | mass | mbarrier
+  double *Us = sm, *V = sm + n3 + 2, *Cf = V + n3, *ms = Cf + 12 * n2;
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(ms + 3 * n);
   const int e = blockIdx.x;
   const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
   const int ecoord[3] = {ex, ey, ez};
   const int edim[3] = {L.nx, L.ny, L.nz};
-  stage(U, u + (long long)e * n3, n3);
-  for (int d = 0; d < 3; ++d) {
-    int c[3] = {ex, ey, ez};
-    c[d] = wrap(ecoord[d] + 1, edim[d]);
-    stage(Cf + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
-          2 * n2);                                                   // tvR, tdR of the right nb
-    c[d] = wrap(ecoord[d] - 1, edim[d]);
-    stage(Cf + d * 4 * n2 + 2 * n2,
-          T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, 2 * n2);
-    stage(ms + d * n, L.mass[d], n);
+  // TMA bulk staging: the element block and the six neighbour-trace segments (2 n^2 doubles,
+  // 16-byte aligned) in 7 copies tracked by one mbarrier.  Element blocks (n^3 doubles, n odd)
+  // alternate 8/16-byte alignment, so a 16-byte aligned superset is copied and U is offset.
+  const double *ue = u + (long long)e * n3;
+  const int pre = (int)((reinterpret_cast<unsigned long long>(ue) >> 3) & 1);
+  const int ucount = (n3 + pre + 1) & ~1;                          // doubles, multiple of 2
+  const bool tail_ok = (long long)e * n3 - pre + ucount <= (long long)L.Ne * n3;
+  double *U = Us + pre;
+  if (threadIdx.x == 0) {
+    mbar_init(mbar, 1);
+    const unsigned tbytes = 16u * n2;                              // 2 n^2 doubles
+    mbar_expect_tx(mbar, (tail_ok ? ucount * 8u : 0u) + 6u * tbytes);
+    if (tail_ok) bulk_g2s(Us, ue - pre, ucount * 8u, mbar);
+    for (int d = 0; d < 3; ++d) {
+      int c[3] = {ex, ey, ez};
+      c[d] = wrap(ecoord[d] + 1, edim[d]);
+      bulk_g2s(Cf + d * 4 * n2, T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2,
+               tbytes, mbar);                                      // tvR, tdR of the right nb
+      c[d] = wrap(ecoord[d] - 1, edim[d]);
+      bulk_g2s(Cf + d * 4 * n2 + 2 * n2,
+               T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + 2 * n2, tbytes,
+               mbar);                                              // tvL, tdL of the left nb
+    }
   }
+  if (!tail_ok) stage(U, ue, n3);
+  for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
   cp_async_wait_all();
+  __syncthreads();
+  mbar_wait(mbar, 0);
   __syncthreads();
   for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
     const int d = t / n2, pp = t - d * n2;
@@ -1450,7 +1493,7 @@ cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, c
 
 static size_t apply_mma_smem(int n) {
   const size_t n2 = (size_t)n * n, n3 = n2 * n;
-  return sizeof(double) * (2 * n3 + 12 * n2 + 3 * n);
+  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2);
 }
 
 cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
