@@ -52,6 +52,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned pha
                  : "=r"(done) : "r"(smem_addr(mbar)), "r"(phase) : "memory");
 }
 
+// Plan a TMA copy of `count` doubles at `src` (8-byte aligned) into the 16-byte aligned staging
+// area `buf` (capacity count + 2): copies the 16-byte aligned superset; returns the pointer to
+// the first element inside `buf`, sets *bytes (0 if the superset would leave [src_base, src_end)).
+struct BulkPlan { double *ptr; unsigned bytes; const double *src; };
+__device__ __forceinline__ BulkPlan bulk_plan(double *buf, const double *src, int count,
+                                              const double *src_end) {
+  const int pre = (int)((reinterpret_cast<unsigned long long>(src) >> 3) & 1);
+  const int cnt = (count + pre + 1) & ~1;
+  BulkPlan b;
+  b.ptr = buf + pre;
+  b.src = src - pre;
+  b.bytes = (b.src + cnt <= src_end) ? 8u * cnt : 0u;
+  return b;
+}
+
 __device__ __forceinline__ void stage(double *dst, const double *src, int count) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) cp_async8(dst + i, src + i);
 }
@@ -753,13 +768,26 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_
   extern __shared__ double sm[];
   const int nf = L.n, n2 = nf * nf, n3 = n2 * nf;
   const int c3 = nc * nc * nc;
-  double *Uc = sm, *T1 = Uc + c3, *T2 = T1 + nf * nc * nc, *U = T2 + nf * nf * nc, *trs = U + n3;
+  const int c3p = (c3 + 3) & ~1;                // staging capacities (16-byte aligned regions)
+  double *Ucs = sm, *Us = Ucs + c3p;
+  double *T1 = Us + ((n3 + 3) & ~1), *T2 = T1 + nf * nc * nc, *trs = T2 + nf * nf * nc;
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * nf);
   const int e = blockIdx.x;
-  stage(Uc, uc + (long long)e * c3, c3);
-  stage(U, uf + (long long)e * n3, n3);
+  const BulkPlan bc = bulk_plan(Ucs, uc + (long long)e * c3, c3, uc + (long long)L.Ne * c3);
+  const BulkPlan bf = bulk_plan(Us, uf + (long long)e * n3, n3, uf + (long long)L.Ne * n3);
+  double *Uc = bc.ptr, *U = bf.ptr;
+  if (threadIdx.x == 0 && (bc.bytes || bf.bytes)) {
+    mbar_init(mbar, 1);
+    mbar_expect_tx(mbar, bc.bytes + bf.bytes);
+    if (bc.bytes) bulk_g2s(Ucs, bc.src, bc.bytes, mbar);
+    if (bf.bytes) bulk_g2s(Us, bf.src, bf.bytes, mbar);
+  }
+  if (!bc.bytes) stage(Uc, uc + (long long)e * c3, c3);
+  if (!bf.bytes) stage(U, uf + (long long)e * n3, n3);
   for (int d = 0; d < 3; ++d) stage(trs + d * 4 * nf, L.tr[d], 4 * nf);
   cp_async_wait_all();
   __syncthreads();
+  if (bc.bytes || bf.bytes) mbar_wait(mbar, 0);
   const Blk BC = {{nc, nc, nc}, {1, nc, nc * nc}};
   const Blk B1 = {{nf, nc, nc}, {1, nf, nf * nc}};
   const Blk B2 = {{nf, nf, nc}, {1, nf, nf * nf}};
@@ -992,12 +1020,24 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
                                                    double *__restrict__ T) {
   extern __shared__ double sm[];
   const int n = L.n, n2 = n * n, n3 = n2 * n;
-  double *U = sm, *trs = sm + n3;
+  double *Us = sm, *trs = sm + n3 + 2;
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * n);
   const int e = blockIdx.x;
-  stage(U, u + (long long)e * n3, n3);
+  const BulkPlan bp = bulk_plan(Us, u + (long long)e * n3, n3, u + (long long)L.Ne * n3);
+  double *U = bp.ptr;
+  if (bp.bytes) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      mbar_expect_tx(mbar, bp.bytes);
+      bulk_g2s(Us, bp.src, bp.bytes, mbar);
+    }
+  } else {
+    stage(U, u + (long long)e * n3, n3);
+  }
   for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
   cp_async_wait_all();
   __syncthreads();
+  if (bp.bytes) mbar_wait(mbar, 0);
   double *Te = T + (long long)e * 12 * n2;
   for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
     const int d = t / n2, p = t - d * n2;
@@ -1386,7 +1426,7 @@ inline int grid_for(long long N, int bs) {
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s) {
   const int n = L.n;
-  const size_t sb = sizeof(double) * ((size_t)n * n * n + 12 * n);
+  const size_t sb = sizeof(double) * ((size_t)n * n * n + 2 + 12 * n + 2);
   if (n <= 20) {
     static size_t configured = 0;
     if (sb > 48 * 1024 && sb > configured) {
@@ -1472,8 +1512,8 @@ cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double
 }
 
 static size_t prolong_traces_smem(int nf, int nc) {
-  return sizeof(double) * ((size_t)nc * nc * nc + (size_t)nf * nc * nc + (size_t)nf * nf * nc +
-                           (size_t)nf * nf * nf + 12 * (size_t)nf);
+  return sizeof(double) * ((size_t)nc * nc * nc + 4 + (size_t)nf * nc * nc + (size_t)nf * nf * nc +
+                           (size_t)nf * nf * nf + 4 + 12 * (size_t)nf + 2);
 }
 
 bool prolong_traces_ok(const LevelDev &Lf, int nc) {
