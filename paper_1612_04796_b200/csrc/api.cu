@@ -561,6 +561,8 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
   if (!dev_ptr || bytes < c->ws_bytes || (reinterpret_cast<size_t>(dev_ptr) & 255))
     return fail(c, PMG_EWORKSPACE, "workspace too small or not 256-byte aligned");
   c->ws = static_cast<char *>(dev_ptr);
+  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);   // graphs baked the old workspace
+  c->graph_cache.clear();
   cudaStream_t s = S(stream);
   auto up = [&](size_t off, const std::vector<double> &v) -> cudaError_t {
     if (v.empty()) return cudaSuccess;

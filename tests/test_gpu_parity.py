@@ -352,3 +352,60 @@ def test_colored_scatter_matches_oracle(name, ne):
         g.pmg_vcycle(ug, _t(f))
         u = mg.vcycle(H, u, f)
         assert _rel(_n(ug), u) <= TOL
+
+
+@pytest.mark.parametrize("name,ne", [("c1", None), ("c2", 3), ("c3", 3), ("c4", 3)])
+def test_pcg_parity_all_configs(name, ne):
+    """MG-CG (Table 1 even rows) on every config family: residual histories to 3 digits."""
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    _, hist_g, ok = g.pcg_solve(ug, _t(f), rtol=1e-10, maxit=80)
+    u, hist_o = mg.pcg(H, f, rtol=1e-10, maxit=80)
+    assert ok and len(hist_g) == len(hist_o)
+    sel = np.array(hist_o) / hist_o[0] >= 1e-9
+    assert np.all(np.abs(hist_g[sel] - np.array(hist_o)[sel]) <= 5e-4 * np.array(hist_o)[sel])
+    assert _rel(_n(ug), u) <= 1e-9
+
+
+def test_vector_helpers_and_coarse_at_c3_size():
+    c = get_config("c3")
+    g = _gpu(c)
+    H = _oracle(c)
+    x = uniform_vector(c.ndofs, 5)
+    y = uniform_vector(c.ndofs, 6)
+    assert abs(g.dot(_t(x), _t(y)) - float(x @ y)) <= 1e-12 * np.abs(x).dot(np.abs(y))
+    xp = _t(x)
+    g.project_mean(xp)
+    assert _rel(_n(xp), x - x.mean()) <= TOL
+    f0 = uniform_vector(H.ndofs(0), 7)         # 32^3 coarse grid (fused 5-kernel path)
+    assert _rel(_n(g.coarse_solve(_t(f0))), H.coarse(f0)) <= TOL
+
+
+def test_single_level_hierarchy_p2():
+    """P = 2: one smoothing level above the P = 1 coarse level (L = 1)."""
+    c = Config("p2", (4, 4, 4), (1.0, 1.0, 1.0), 2, 1, OverlapSpec(1, 0.5, 0))
+    g = _gpu(c)
+    H = MFHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    u = np.zeros(c.ndofs)
+    for _ in range(3):
+        g.pmg_vcycle(ug, _t(f))
+        u = mg.vcycle(H, u, f)
+    assert _rel(_n(ug), u) <= TOL
+
+
+def test_workspace_and_state_errors():
+    from paper_1612_04796_b200 import DG, PMGError
+    from paper_1612_04796_b200.binding import lib
+    import ctypes as C
+    g = DG((4, 4, 4), (1, 1, 1), 4, 0, overlap=OverlapSpec(0, 1, 0), bind=False)
+    small = torch.empty(1024, dtype=torch.uint8, device="cuda")
+    rc = lib.dg_bind_workspace(g._c, C.c_void_p(small.data_ptr()), 1024, None)
+    assert rc == 5                                   # PMG_EWORKSPACE
+    u = torch.zeros(g.ndofs(), dtype=torch.float64, device="cuda")
+    with pytest.raises(PMGError):
+        g.apply(u)                                   # workspace not bound -> PMG_ESTATE
