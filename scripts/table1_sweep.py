@@ -62,11 +62,22 @@ def run_case(basis, solver, ov, P, ne, maxit=60):
     dt = time.perf_counter() - t0
     n = len(hist) - 1
     rho = (hist[-1] / hist[0]) ** (1.0 / n) if n > 0 and hist[-1] > 0 else float("nan")
+    # t_C: device time of one V(1,1) cycle (graph replay), tau10 = -10 t_C / lg rho per unknown
+    # (the paper: ~3.5 us per unknown on one 3.1 GHz Broadwell core)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.pmg_vcycle(u, f)
+    e0.record()
+    for _ in range(5):
+        g.pmg_vcycle(u, f)
+    e1.record()
+    torch.cuda.synchronize()
+    t_c = e0.elapsed_time(e1) / 5 / 1e3
+    tau10 = -10.0 * t_c / math.log10(rho) / N if 0 < rho < 1 else float("nan")
     no = [g.level_overlap(l)[0][0] for l in range(1, g.L + 1)]
     del g
     torch.cuda.empty_cache()
     return {"rho": rho, "lg": -math.log10(rho) if rho > 0 else None, "cycles": n, "hist": hist,
-            "n_o": no, "dofs": N, "seconds": dt}
+            "n_o": no, "dofs": N, "seconds": dt, "t_cycle_s": t_c, "tau10_ns_per_dof": tau10 * 1e9}
 
 
 def main():
@@ -80,9 +91,9 @@ def main():
             ne = 128 // P
             res = run_case(basis, solver, ov, P, ne)
             out["%d/%d" % (row, P)] = dict(res, paper=paper[Ps.index(P)], basis=basis, solver=solver)
-            print("row %2d P=%2d ne=%2d  -lg rho = %5.2f (paper %4.2f)  cycles %3d  n_o %s  %.1fs" % (
+            print("row %2d P=%2d ne=%2d  -lg rho = %5.2f (paper %4.2f)  cycles %3d  n_o %s  t_C %.3f ms  tau10 %.2f ns/DOF" % (
                 row, P, ne, res["lg"] or float("nan"), paper[Ps.index(P)], res["cycles"], res["n_o"],
-                res["seconds"]), flush=True)
+                res["t_cycle_s"] * 1e3, res["tau10_ns_per_dof"]), flush=True)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "%s_table1_gpu.json" % tag), "w") as fh:
         json.dump(out, fh, indent=1)
