@@ -11,6 +11,9 @@
 
 namespace pmg {
 
+#ifndef PMG_LINES
+#define PMG_LINES mma_lines_p
+#endif
 #ifndef FDM_BIG_THREADS
 #define FDM_BIG_THREADS 256
 #endif
@@ -365,6 +368,107 @@ __device__ __forceinline__ void mma_lines_t(const double *X, const Blk &B, const
   }
 }
 
+// Software-pipelined variant: one 8-column tile per step, the DMMAs of tile i+1 are issued
+// before the epilogue of tile i, so the epilogue's shared-memory stores and index math fill the
+// DMMA pipe's 16-cycle issue gaps instead of idling it (ping-pong accumulators c0/c1).
+template <int DIR, int KS, int MT, bool TAIL, class Epi>
+__device__ __forceinline__ void mma_lines_p(const double *X, const Blk &B, const LineSpec &ls,
+                                            Epi &epi) {
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  const int mo = ls.mo, mk = ls.mk, kt = ls.mk + ls.next;
+  const int mp = B.m[PD], mq = B.m[QD];
+  const int ncol = mp * mq;
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)mp + 1u;
+  const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ntiles = (ncol + 7) >> 3;
+  if (warp >= ntiles) return;
+  double a[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      a[mt][ks] = (o < mo && k < kt) ? ls.Amat[o * ls.ao + k * ls.ak] : 0.0;
+    }
+  double at[TAIL ? KS : 1];
+  if (TAIL) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = ks * 4 + t;
+      at[ks] = k < kt ? ls.Amat[(8 * MT) * ls.ao + k * ls.ak] : 0.0;
+    }
+  }
+  int koff[KS];
+  bool kext[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = min(ks * 4 + t, kt - 1);
+    kext[ks] = k >= mk;
+    koff[ks] = kext[ks] ? (k - mk) * ls.esr : k * so;
+  }
+  // compute one tile into (c, tl); returns the column of the B loads (for the tail row)
+  auto compute = [&](int tile, double (&c)[MT][2], double &tl, int &pb, int &qb) {
+    const int nb = min(tile * 8 + g, ncol - 1);
+    qb = __umulhi((unsigned)nb, magic);
+    pb = nb - qb * mp;
+    const double *xb = X + pb * sp + qb * sq;
+    const double *eb = ls.Ext ? ls.Ext + pb * ls.esp + qb * ls.esq : X;
+    double b[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) b[ks] = (kext[ks] ? eb : xb)[koff[ks]];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { c[mt][0] = 0.0; c[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][0], c[mt][1], a[mt][ks], b[ks]);
+    tl = 0.0;
+    if (TAIL) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) tl = fma(at[ks], b[ks], tl);
+      tl += __shfl_xor_sync(0xffffffffu, tl, 1);
+      tl += __shfl_xor_sync(0xffffffffu, tl, 2);
+    }
+  };
+  auto epilogue = [&](int tile, const double (&c)[MT][2], double tl, int pb, int qb) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tile * 8 + 2 * t + j;
+      if (n >= ncol) continue;
+      const int q = __umulhi((unsigned)n, magic), p = n - q * mp;
+      const double cf = epi.template col<DIR>(p, q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o < mo) epi.template put<DIR>(o, p, q, cf, c[mt][j]);
+      }
+    }
+    if (TAIL && t == 0 && tile * 8 + g < ncol) {
+      const double cf = epi.template col<DIR>(pb, qb);
+      epi.template put<DIR>(8 * MT, pb, qb, cf, tl);
+    }
+  };
+  double c0[MT][2], c1[MT][2], tl0, tl1;
+  int pb0, qb0, pb1, qb1;
+  int tile = warp;
+  compute(tile, c0, tl0, pb0, qb0);
+  for (;;) {
+    const int t1 = tile + nw;
+    if (t1 < ntiles) compute(t1, c1, tl1, pb1, qb1);
+    __syncwarp();
+    epilogue(tile, c0, tl0, pb0, qb0);
+    if (t1 >= ntiles) break;
+    const int t2 = t1 + nw;
+    if (t2 < ntiles) compute(t2, c0, tl0, pb0, qb0);
+    __syncwarp();
+    epilogue(t1, c1, tl1, pb1, qb1);
+    if (t2 >= ntiles) break;
+    tile = t2;
+  }
+}
+
 // Supported (KS, MT) tiles; any request is served by the smallest supported tile that covers
 // it (A is zero padded, so a larger tile is correct, only wasteful).
 template <int DIR, int KSMAX, class Epi>
@@ -373,13 +477,13 @@ __device__ void mma_lines_gen(const double *X, const Blk &B, const LineSpec &ls,
   if (ls.mo > 8 && (ls.mo & 7) == 1) {           // 8k+1 rows: DMMA for 8k, FMA tail row
     const int MTT = ls.mo >> 3;
 #define PMG_TTILE(ks, mt) \
-    if (ks <= KSMAX && KS <= ks && MTT == mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt, true>(X, B, ls, epi); return; }
+    if (ks <= KSMAX && KS <= ks && MTT == mt) { PMG_LINES<DIR, (ks <= KSMAX ? ks : 1), mt, true>(X, B, ls, epi); return; }
     PMG_TTILE(2, 1) PMG_TTILE(3, 1) PMG_TTILE(4, 1) PMG_TTILE(5, 1) PMG_TTILE(3, 2) PMG_TTILE(5, 2)
     PMG_TTILE(6, 2)
 #undef PMG_TTILE
   }
 #define PMG_TILE(ks, mt) \
-  if (ks <= KSMAX && KS <= ks && MT <= mt) { mma_lines_t<DIR, (ks <= KSMAX ? ks : 1), mt, false>(X, B, ls, epi); return; }
+  if (ks <= KSMAX && KS <= ks && MT <= mt) { PMG_LINES<DIR, (ks <= KSMAX ? ks : 1), mt, false>(X, B, ls, epi); return; }
   PMG_TILE(1, 1) PMG_TILE(2, 1) PMG_TILE(2, 2) PMG_TILE(3, 1) PMG_TILE(3, 2) PMG_TILE(3, 3)
   PMG_TILE(4, 2) PMG_TILE(5, 2) PMG_TILE(5, 3) PMG_TILE(6, 3) PMG_TILE(7, 4) PMG_TILE(8, 4)
 #undef PMG_TILE
