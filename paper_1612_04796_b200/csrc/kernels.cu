@@ -636,6 +636,9 @@ template <int KSMAX>
 __device__ __forceinline__ bool fdm_z_fused(double *X, const Blk &B, const double *S,
                                             const double *const *lam) {
   const int KS = (B.m[2] + 3) >> 2;
+#ifdef PMG_NO_ZFUSE
+  return false;
+#endif
   if (KS <= 1) { fdm_z_fused_t<1, 1>(X, B, S, lam); return true; }
   if (KS <= 2) { fdm_z_fused_t<2, 1>(X, B, S, lam); return true; }
   if (KSMAX >= 4 && KS <= 4) { fdm_z_fused_t<(KSMAX >= 4 ? 4 : 1), 2>(X, B, S, lam); return true; }
