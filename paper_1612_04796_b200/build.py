@@ -7,7 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmgdg.so")
-SOURCES = ["api.cu", "kernels.cu", "setup.cpp", "probe.cu"]
+SOURCES = ["api.cu", "kern_fdm.cu", "kern_apply.cu", "kern_xfer.cu", "kern_global.cu", "kern_misc.cu",
+           "setup.cpp", "probe.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
@@ -24,14 +25,28 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
-    for src in SOURCES:
+
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    headers.append(os.path.join(ROOT, "include", "pmg_dg.h"))
+
+    def compile_one(src):
         obj = os.path.join(HERE, "build", src + ".o")
+        if not force and os.path.exists(obj):
+            t = os.path.getmtime(obj)
+            if all(os.path.getmtime(d) <= t for d in headers + [os.path.join(CSRC, src)]):
+                return obj, subprocess.CompletedProcess([], 0, "", "")
         cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-x", "cu"] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units compile in parallel (the kernel files dominate the build time)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for src, (obj, r) in zip(SOURCES, results):
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed on " + src)

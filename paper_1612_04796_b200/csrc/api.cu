@@ -499,9 +499,11 @@ int dg_schwarz_setup(dg_ctx *c, int mode, double value, int floor_layers) {
         for (int b = 0; b < m; ++b) Ls[a * m + b] = op.L[size_t(ga) * N1 + (n - no + b) % N1];
       }
       std::vector<ld> lam, Sv;
-      pmg::gen_eig(m, Ls, Ms, lam, Sv);
-      h.lam_min[d] = lam[0];
-      h.lam_max[d] = lam[m - 1];
+      // odd windows (always, for n = 2^l + 1): exact-parity eigenvectors, even modes first
+      if (m & 1) pmg::gen_eig_parity(m, Ls, Ms, lam, Sv);
+      else pmg::gen_eig(m, Ls, Ms, lam, Sv);
+      h.lam_min[d] = *std::min_element(lam.begin(), lam.end());
+      h.lam_max[d] = *std::max_element(lam.begin(), lam.end());
       h.S[d] = to_d(Sv);
       h.lam[d] = to_d(lam);
       h.W[d] = to_d(pmg::hat_weights(h.basis, h.ov[d]));

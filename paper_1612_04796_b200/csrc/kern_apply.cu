@@ -1,0 +1,355 @@
+// Matrix-free IP-DG operator apply / residual (+ fused restriction) and face traces.
+// arXiv:1612.04796; PAPER.md line numbers cited per kernel.
+#include <algorithm>
+
+#include "kcommon.cuh"
+
+namespace pmg {
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// Face traces (value and normal derivative on both faces of every direction) — the data the
+// rank-2 neighbour couplings of Eq. 7's block-tridiagonal L_* need.
+__global__ void k_traces(LevelDev L, const double *__restrict__ u, double *__restrict__ T) {
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int e = blockIdx.x;
+  const double *ue = u + (long long)e * n3;
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = L.tr[d];
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = __ldg(ue + base + i * stride);
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
+// Operator apply v = A u (Eq. 7) or residual r = f - A u (Eq. 8), sum-factorised per element.
+__global__ void k_apply(LevelDev L, const double *__restrict__ u, const double *__restrict__ T,
+                        const double *__restrict__ f, double *__restrict__ out) {
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  const int e = blockIdx.x;
+  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
+  const int ecoord[3] = {ex, ey, ez};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  int nbL[3], nbR[3];
+  for (int d = 0; d < 3; ++d) {
+    int c[3] = {ex, ey, ez};
+    c[d] = wrap(ecoord[d] - 1, edim[d]);
+    nbL[d] = c[0] + L.nx * (c[1] + L.ny * c[2]);
+    c[d] = wrap(ecoord[d] + 1, edim[d]);
+    nbR[d] = c[0] + L.nx * (c[1] + L.ny * c[2]);
+  }
+  const double *ue = u + (long long)e * n3;
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int i = t % n, j = (t / n) % n, k = t / n2;
+    const int idx[3] = {i, j, k};
+    const int pface[3] = {j + n * k, i + n * k, i + n * j};
+    const int stride[3] = {1, n, n2};
+    double s[3];
+    for (int d = 0; d < 3; ++d) {
+      const int id = idx[d];
+      const double *Dr = L.D[d] + id * n;
+      const double *line = ue + (t - id * stride[d]);
+      double acc = 0;
+      for (int q = 0; q < n; ++q) acc += Dr[q] * __ldg(line + q * stride[d]);
+      const double *TR = T + ((long long)nbR[d] * 3 + d) * 4 * n2;
+      const double *TL = T + ((long long)nbL[d] * 3 + d) * 4 * n2;
+      const double tvR = TR[pface[d]], tdR = TR[n2 + pface[d]];
+      const double tvL = TL[2 * n2 + pface[d]], tdL = TL[3 * n2 + pface[d]];
+      const double *tr = L.tr[d];
+      const double mu = L.mu[d];
+      acc += tr[id] * (-0.5 * tdR - mu * tvR) + tr[n + id] * (0.5 * tvR)
+           + tr[2 * n + id] * (0.5 * tdL - mu * tvL) + tr[3 * n + id] * (-0.5 * tvL);
+      s[d] = acc;
+    }
+    const double mx = L.mass[0][i], my = L.mass[1][j], mz = L.mass[2][k];
+    const double v = mz * my * s[0] + mz * mx * s[1] + my * mx * s[2];
+    const long long g = (long long)e * n3 + t;
+    out[g] = f ? f[g] - v : v;
+  }
+}
+
+// smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
+// Per direction d the line GEMM is  V += M_p M_q [D | a ap b bp] [U-lines ; c1 c2 c3 c4]  where
+// c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
+// c1 = -tdR/2 - mu tvR, c2 = tvR/2, c3 = tdL/2 - mu tvL, c4 = -tvL/2.
+// NT = n (compile time, n = 2^l + 1 or 2), NC = (n + 1) / 2 the next-coarser n (fused restriction)
+template <int NT>
+__global__ void __launch_bounds__(NT <= 9 ? 128 : 256, NT <= 9 ? 8 : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+                                                      const double *__restrict__ T,
+                                                      const double *__restrict__ f,
+                                                      double *__restrict__ out,
+                                                      const double *__restrict__ restrict_I,
+                                                      double *__restrict__ fc) {
+  extern __shared__ double sm[];
+  constexpr int n = NT, n2 = n * n, n3 = n2 * n;
+  constexpr int NC = NT > 2 ? (NT + 1) / 2 : 1;
+  // smem: U staging (n^3 + 2, 16-byte aligned superset of the element) | V | Cf | mass | mbarrier
+  double *Us = sm, *V = sm + n3 + 2, *Cf = V + n3, *ms = Cf + 12 * n2;
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(ms + 3 * n);
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  const unsigned tbytes = 16u * n2;                                // 2 n^2 doubles per segment
+  // Persistent: CTA b handles elements b, b + grid, ...  While element e is computed, the next
+  // element's block, its neighbour-trace segments and e's f block are prefetched into L2
+  // (cp.async.bulk.prefetch), so the HBM stream keeps running under the DMMA passes and the
+  // next TMA load and the epilogue's f reads are served from L2.
+  auto trace_src = [&](int e, int d, int side) {                   // side 0: right nb (tvR, tdR)
+    int c[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+    c[d] = wrap(c[d] + (side ? -1 : 1), edim[d]);
+    return T + ((long long)(c[0] + L.nx * (c[1] + L.ny * c[2])) * 3 + d) * 4 * n2 + side * 2 * n2;
+  };
+  auto u_plan = [&](int e, int &pre, int &ucount) {
+    const double *ue = u + (long long)e * n3;
+    pre = (int)((reinterpret_cast<unsigned long long>(ue) >> 3) & 1);
+    ucount = (n3 + pre + 1) & ~1;                                  // doubles, multiple of 2
+    return (long long)e * n3 - pre + ucount <= (long long)L.Ne * n3;
+  };
+  if (threadIdx.x == 0) mbar_init(mbar, 1);
+  for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
+  __syncthreads();
+  unsigned phase = 0;
+  for (int e = blockIdx.x; e < L.Ne; e += gridDim.x, phase ^= 1u) {
+    // TMA bulk staging: the element block and the six neighbour-trace segments (2 n^2 doubles,
+    // 16-byte aligned) in 7 copies tracked by one mbarrier.  Element blocks (n^3 doubles, n odd)
+    // alternate 8/16-byte alignment, so a 16-byte aligned superset is copied and U is offset.
+    const double *ue = u + (long long)e * n3;
+    int pre, ucount;
+    const bool tail_ok = u_plan(e, pre, ucount);
+    double *U = Us + pre;
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(mbar, (tail_ok ? ucount * 8u : 0u) + 6u * tbytes);
+      if (tail_ok) bulk_g2s(Us, ue - pre, ucount * 8u, mbar);
+      for (int d = 0; d < 3; ++d) {
+        bulk_g2s(Cf + d * 4 * n2, trace_src(e, d, 0), tbytes, mbar);
+        bulk_g2s(Cf + d * 4 * n2 + 2 * n2, trace_src(e, d, 1), tbytes, mbar);
+      }
+      const int en = e + gridDim.x;
+      if (en < L.Ne) {
+        int pn, cn;
+        if (u_plan(en, pn, cn)) prefetch_l2(u + (long long)en * n3 - pn, cn * 8u);
+        for (int d = 0; d < 3; ++d) {
+          prefetch_l2(trace_src(en, d, 0), tbytes);
+          prefetch_l2(trace_src(en, d, 1), tbytes);
+        }
+      }
+      if (f) {
+        const double *fe = f + (long long)e * n3;
+        const int fp = (int)((reinterpret_cast<unsigned long long>(fe) >> 3) & 1);
+        const int fcnt = (n3 + fp + 1) & ~1;
+        if ((long long)e * n3 - fp + fcnt <= (long long)L.Ne * n3) prefetch_l2(fe - fp, fcnt * 8u);
+      }
+    }
+    if (!tail_ok) stage(U, ue, n3);
+    cp_async_wait_all();
+    __syncthreads();
+    mbar_wait(mbar, phase);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+      const int d = t / n2, pp = t - d * n2;
+      double *C = Cf + d * 4 * n2 + pp;
+      const double mu = L.mu[d];
+      const double tvR = C[0], tdR = C[n2], tvL = C[2 * n2], tdL = C[3 * n2];
+      C[0] = -0.5 * tdR - mu * tvR;
+      C[n2] = 0.5 * tvR;
+      C[2 * n2] = 0.5 * tdL - mu * tvL;
+      C[3 * n2] = -0.5 * tvL;
+    }
+    __syncthreads();
+    const Blk B = {{n, n, n}, {1, n, n2}};
+    EpiAcc acc{V, B, true};
+    LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
+    mma_lines_ct<0, n, n + 4>(U, B, lx, acc); __syncthreads();
+    acc.first = false;
+    LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
+    mma_lines_ct<1, n, n + 4>(U, B, ly, acc); __syncthreads();
+    LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
+    mma_lines_ct<2, n, n + 4>(U, B, lz, acc); __syncthreads();
+    // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism
+    const long long g0 = (long long)e * n3;
+    constexpr int UNR = 4;
+    for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
+      double fv[UNR];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int t = t0 + q * blockDim.x;
+        fv[q] = (f && t < n3) ? __ldg(f + g0 + t) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int t = t0 + q * blockDim.x;
+        if (t >= n3) break;
+        const int i = t % n, j = (t / n) % n, k = t / n2;
+        const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
+        const double rr = f ? fv[q] - v : v;
+        if (restrict_I) V[t] = rr;
+        else out[g0 + t] = rr;
+      }
+    }
+    if (NT > 2 && restrict_I) {
+      // fused residual restriction f_c = (I^T (x) I^T (x) I^T) r (Alg. 1 l.292): r stays in V;
+      // x pass (n -> nc) into U, y pass into Cf, z pass straight to the coarse vector
+      __syncthreads();
+      constexpr int nc = NC;
+      const Blk T1 = {{nc, n, n}, {1, nc, nc * n}};
+      const Blk T2 = {{nc, nc, n}, {1, nc, nc * nc}};
+      const Blk FC = {{nc, nc, nc}, {1, nc, nc * nc}};
+      const LineSpec rx = {nc, n, restrict_I, 1, nc, nullptr, 0, 0, 0, 0};
+      EpiStore s1{U, T1};
+      mma_lines_ct<0, NC, n>(V, B, rx, s1); __syncthreads();
+      EpiStore s2{Cf, T2};
+      mma_lines_ct<1, NC, n>(U, T1, rx, s2); __syncthreads();
+      EpiStore s3{fc + (long long)e * nc * nc * nc, FC};
+      mma_lines_ct<2, NC, n>(Cf, T2, rx, s3);
+    }
+    __syncthreads();                   // U, V, Cf are reused by the next element
+  }
+}
+
+// Face traces with the element staged in shared memory (coalesced loads).
+__global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__restrict__ u,
+                                                   double *__restrict__ T) {
+  extern __shared__ double sm[];
+  const int n = L.n, n2 = n * n, n3 = n2 * n;
+  double *Us = sm, *trs = sm + n3 + 2;
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * n);
+  const int e = blockIdx.x;
+  const BulkPlan bp = bulk_plan(Us, u + (long long)e * n3, n3, u + (long long)L.Ne * n3);
+  double *U = bp.ptr;
+  if (bp.bytes) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      mbar_expect_tx(mbar, bp.bytes);
+      bulk_g2s(Us, bp.src, bp.bytes, mbar);
+    }
+  } else {
+    stage(U, u + (long long)e * n3, n3);
+  }
+  for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
+  cp_async_wait_all();
+  __syncthreads();
+  if (bp.bytes) mbar_wait(mbar, 0);
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = U[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s) {
+  const int n = L.n;
+  const size_t sb = sizeof(double) * ((size_t)n * n * n + 2 + 12 * n + 2);
+  if (n <= 20) {
+    static size_t configured = 0;
+    if (sb > 48 * 1024 && sb > configured) {
+      cudaFuncSetAttribute(k_traces_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      configured = sb;
+    }
+    k_traces_sm<<<L.Ne, 256, sb, s>>>(L, u, T);
+  } else {
+    k_traces<<<L.Ne, 128, 0, s>>>(L, u, T);
+  }
+  return cudaGetLastError();
+}
+static void configure_smem() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const int mx = 227 * 1024;
+  cudaFuncSetAttribute(k_apply_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_apply_mma<17>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
+static size_t apply_pipe_smem(int n) {
+  const size_t n2 = (size_t)n * n, n3 = n2 * n;
+  return sizeof(double) * (3 * n3 + 24 * n2 + 3 * n);
+}
+
+bool apply_pipe_ok(const LevelDev &L) { return L.n == 3 || L.n == 5 || L.n == 9 || L.n == 17; }
+
+static size_t apply_mma_smem(int n) {
+  const size_t n2 = (size_t)n * n, n3 = n2 * n;
+  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2);
+}
+
+template <int NT>
+static int apply_grid(size_t sb, long long Ne) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_mma<NT>, NT <= 9 ? 128 : 256, sb);
+    occ = std::max(occ, 1);
+  }
+  return (int)std::min<long long>(Ne, (long long)occ * num_sms());
+}
+
+template <int NT>
+static void launch_apply_nt(const LevelDev &L, const double *u, const double *T, const double *f,
+                            double *out, const double *I, double *fc, cudaStream_t s) {
+  // persistent grid: as many CTAs as fit on the device at once (occupancy x SMs), capped at Ne
+  const size_t sb = apply_mma_smem(NT);
+  const int threads = NT <= 9 ? 128 : 256;
+  k_apply_mma<NT><<<apply_grid<NT>(sb, L.Ne), threads, sb, s>>>(L, u, T, f, out, I, fc);
+}
+
+bool apply_nt_ok(int n) { return n == 2 || n == 3 || n == 5 || n == 9 || n == 17; }
+
+cudaError_t launch_apply_pipe(const LevelDev &L, const double *u, const double *T, const double *f,
+                              double *out, const double *I, int nc, double *fc, cudaStream_t s) {
+  configure_smem();
+  if (I && nc != (L.n + 1) / 2) return cudaErrorInvalidValue;
+  switch (L.n) {
+    case 2: launch_apply_nt<2>(L, u, T, f, out, nullptr, nullptr, s); break;
+    case 3: launch_apply_nt<3>(L, u, T, f, out, I, fc, s); break;
+    case 5: launch_apply_nt<5>(L, u, T, f, out, I, fc, s); break;
+    case 9: launch_apply_nt<9>(L, u, T, f, out, I, fc, s); break;
+    case 17: launch_apply_nt<17>(L, u, T, f, out, I, fc, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, const double *f,
+                         double *out, cudaStream_t s) {
+  const int n = L.n;
+
+  if (n <= 17) {
+    return launch_apply_pipe(L, u, T, f, out, nullptr, 0, nullptr, s);
+  } else {
+    k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
+  }
+  return cudaGetLastError();
+}
+}  // namespace pmg

@@ -1,0 +1,467 @@
+// Deterministic fold, coarse pseudo-inverse, reductions, PCG vector ops, RHS.
+// arXiv:1612.04796; PAPER.md line numbers cited per kernel.
+#include <algorithm>
+
+#include "kcommon.cuh"
+
+namespace pmg {
+namespace {
+
+// Register-only fold: one thread per DOF issues all (up to 27) predicated loads of the
+// weighted window values that cover it before summing them in a fixed order -> maximal
+// memory-level parallelism, deterministic result.  NT = compile-time n (fast index math).
+template <int NT, bool TR>
+__global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restrict__ Z,
+                                               double *__restrict__ u, int zero,
+                                               double *__restrict__ T) {
+  extern __shared__ double sm[];          // TR: the folded element (n^3) + trace table (12 n)
+  const int n = NT > 0 ? NT : L.n;
+  const int n3 = n * n * n;
+  const int mx = L.m[0], my = L.m[1];
+  const long long Mw = L.Mw;
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  int se[3][3];                       // source subdomain coordinate per direction: o = -1, 0, +1
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
+  const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
+  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+    const int i = t % n, j = (t / n) % n, k = t / (n * n);
+    const int idx[3] = {i, j, k};
+    const int nod[3] = {no0, no1, no2};
+    bool v[3][3];
+    int wi[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int no = nod[d], id = idx[d];
+      v[d][0] = id < no;        wi[d][0] = no + n + id;     // left-neighbour subdomain
+      v[d][1] = true;           wi[d][1] = no + id;         // own subdomain
+      v[d][2] = id >= n - no;   wi[d][2] = id - (n - no);   // right-neighbour subdomain
+    }
+    const long long g = (long long)e * n3 + t;
+    double du = zero ? 0.0 : u[g];
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      if (!v[2][oz]) continue;
+      double z[9];
+#pragma unroll
+      for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          const bool ok = v[0][ox] && v[1][oy];
+          const long long sidx = se[0][ox] + L.nx * (se[1][oy] + (long long)L.ny * se[2][oz]);
+          z[ox + 3 * oy] = ok ? __ldg(Z + sidx * Mw + wi[0][ox] + mx * (wi[1][oy] + my * wi[2][oz])) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) du += z[q];
+    }
+    u[g] = du;
+    if (TR) sm[t] = du;
+  }
+  if (!TR) return;
+  // fused trace pass of the following residual: face values / derivatives of the new u
+  const int n2 = n * n;
+  double *trs = sm + n3;
+  for (int d = 0; d < 3; ++d)
+    for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) trs[d * 4 * n + i] = L.tr[d][i];
+  __syncthreads();
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = sm[base + i * stride];
+      rv += tr[i] * v;
+      rder += tr[n + i] * v;
+      lv += tr[2 * n + i] * v;
+      lder += tr[3 * n + i] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Coarse level (P_0 = 1): u_0 = A_0^+ f_0 by global fast diagonalisation on the periodic
+// (2nx, 2ny, 2nz) grid with the constant mode removed (Alg. 1 l.295).
+__global__ void k_coarse_gather(int nx, int ny, int nz, const double *__restrict__ f0,
+                                const double *__restrict__ mean, double *__restrict__ G) {
+  const long long N = 8LL * nx * ny * nz;
+  const double mu = *mean;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int node = g & 7;
+    const long long e = g >> 3;
+    const int i = node & 1, j = (node >> 1) & 1, k = node >> 2;
+    const int ex = e % nx, ey = (e / nx) % ny, ez = e / ((long long)nx * ny);
+    const long long X = 2 * ex + i, Y = 2 * ey + j, Z = 2 * ez + k;
+    G[X + 2LL * nx * (Y + 2LL * ny * Z)] = f0[g] - mu;
+  }
+}
+
+__global__ void k_lex_contract(CoarseDev C, int axis, int forward, const double *__restrict__ in,
+                               double *__restrict__ out) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  const int Gd = C.G[axis];
+  const long long st = axis == 0 ? 1 : (axis == 1 ? C.G[0] : (long long)C.G[0] * C.G[1]);
+  const double *S = C.S[axis];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int o = (g / st) % Gd;
+    const double *src = in + (g - o * st);
+    double acc = 0;
+    if (forward) for (int k = 0; k < Gd; ++k) acc += S[k * Gd + o] * src[k * st];
+    else for (int k = 0; k < Gd; ++k) acc += S[o * Gd + k] * src[k * st];
+    out[g] = acc;
+  }
+}
+
+__global__ void k_coarse_divide(CoarseDev C, double *__restrict__ G) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int a = g % C.G[0], b = (g / C.G[0]) % C.G[1], c = g / ((long long)C.G[0] * C.G[1]);
+    // eigenvalue index 0 is the (exactly zero) constant mode in every direction
+    G[g] = (a == 0 && b == 0 && c == 0) ? 0.0 : G[g] / (C.lam[0][a] + C.lam[1][b] + C.lam[2][c]);
+  }
+}
+
+__global__ void k_coarse_scatter(int nx, int ny, int nz, const double *__restrict__ G,
+                                 const double *__restrict__ mean, double *__restrict__ u0) {
+  const long long N = 8LL * nx * ny * nz;
+  const double mu = *mean;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int node = g & 7;
+    const long long e = g >> 3;
+    const int i = node & 1, j = (node >> 1) & 1, k = node >> 2;
+    const int ex = e % nx, ey = (e / nx) % ny, ez = e / ((long long)nx * ny);
+    const long long X = 2 * ex + i, Y = 2 * ey + j, Z = 2 * ez + k;
+    u0[g] = G[X + 2LL * nx * (Y + 2LL * ny * Z)] - mu;
+  }
+}
+
+// Fused coarse-solve passes.  At P_0 = 1 on a uniform grid the 1D mass matrices are multiples of
+// the identity (w = (1,1)), so dropping the (exactly constant) null mode of the fast
+// diagonalisation already realises the Euclidean projection of f_0 and returns a Euclidean
+// mean-free u_0: A_0^+ f_0 = S (Lambda^+) S^T f_0 with no separate mean reductions.
+__device__ __forceinline__ long long coarse_elem_index(int nx, int ny, int X, int Y, int Z) {
+  const long long e = (X >> 1) + (long long)nx * ((Y >> 1) + (long long)ny * (Z >> 1));
+  return e * 8 + (X & 1) + 2 * (Y & 1) + 4 * (Z & 1);
+}
+
+// x-forward pass reading f_0 in element-major order: G[X',Y,Z] = sum_X S0x[X][X'] f0(X,Y,Z)
+__global__ void k_coarse_xf(CoarseDev C, int nx, int ny, const double *__restrict__ f0,
+                            double *__restrict__ G) {
+  const int Gx = C.G[0], Gy = C.G[1];
+  const long long N = (long long)Gx * Gy * C.G[2];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int o = g % Gx, Y = (g / Gx) % Gy, Z = g / ((long long)Gx * Gy);
+    double acc = 0;
+    for (int X = 0; X < Gx; ++X) acc += C.S[0][X * Gx + o] * __ldg(f0 + coarse_elem_index(nx, ny, X, Y, Z));
+    G[g] = acc;
+  }
+}
+
+// z column (one warp per column, lane = z index): forward S_z^T, divide by the eigenvalue
+// sums (null mode -> 0), backward S_z; column values exchanged with warp shuffles.
+__global__ void k_coarse_z(CoarseDev C, double *__restrict__ G) {
+  const int Gx = C.G[0], Gy = C.G[1], Gz = C.G[2];
+  const long long cols = (long long)Gx * Gy;
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const double *S = C.S[2];
+  for (long long cidx = w0; cidx < cols; cidx += nw) {
+    const int a = cidx % Gx, b = cidx / Gx;
+    const double v = lane < Gz ? G[cidx + lane * cols] : 0.0;
+    double acc = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double vk = __shfl_sync(0xffffffffu, v, k);
+      if (lane < Gz) acc += S[k * Gz + lane] * vk;
+    }
+    double w = 0.0;
+    if (lane < Gz && !(a == 0 && b == 0 && lane == 0))
+      w = acc / (C.lam[0][a] + C.lam[1][b] + C.lam[2][lane]);
+    double out = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double wk = __shfl_sync(0xffffffffu, w, k);
+      if (lane < Gz) out += S[lane * Gz + k] * wk;
+    }
+    if (lane < Gz) G[cidx + lane * cols] = out;
+  }
+}
+
+// x-backward pass writing u_0 in element-major order
+__global__ void k_coarse_xb(CoarseDev C, int nx, int ny, const double *__restrict__ G,
+                            double *__restrict__ u0) {
+  const int Gx = C.G[0], Gy = C.G[1];
+  const long long N = (long long)Gx * Gy * C.G[2];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int X = g % Gx, Y = (g / Gx) % Gy, Z = g / ((long long)Gx * Gy);
+    const double *row = G + (g - X);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += C.S[0][X * Gx + k] * row[k];
+    u0[coarse_elem_index(nx, ny, X, Y, Z)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic reductions: fixed grid for a given N, fixed per-thread order, fixed tree.
+constexpr int RB = 256;
+constexpr int RMAX = 1184;   // 8 x 148 SMs
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[RB / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < RB / 32 ? sh[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  }
+  __syncthreads();
+  return v;   // valid in thread 0
+}
+
+template <int MODE>
+__global__ void k_partial(const double *__restrict__ x, const double *__restrict__ y,
+                          const double *__restrict__ z, long long N, double *__restrict__ part) {
+  // MODE 0: sum x;  1: x.y;  2: (x.(y - z), x.y) two outputs
+  double a = 0, b = 0;
+  for (long long g = blockIdx.x * (long long)RB + threadIdx.x; g < N; g += (long long)gridDim.x * RB) {
+    if (MODE == 0) a += x[g];
+    else if (MODE == 1) a += x[g] * y[g];
+    else { a += x[g] * (y[g] - z[g]); b += x[g] * y[g]; }
+  }
+  a = block_sum(a);
+  if (MODE == 2) b = block_sum(b);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = a;
+    if (MODE == 2) part[gridDim.x + blockIdx.x] = b;
+  }
+}
+
+// final stage: op 0 -> out[0] = scale * sum; op 1 -> pq & alpha; op 2 -> zr / beta
+__global__ void k_final(const double *__restrict__ part, int nb, int nout, double *__restrict__ out,
+                        double scale, int op) {
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < nb; i += RB) {
+    a += part[i];
+    if (nout == 2) b += part[nb + i];
+  }
+  a = block_sum(a);
+  if (nout == 2) b = block_sum(b);
+  if (threadIdx.x == 0) {
+    if (op == 0) out[0] = scale * a;
+    else if (op == 1) { out[1] = a; out[5] = out[0] / a; }                 // pq, alpha = zr/pq
+    else if (op == 2) { out[3] = a; out[4] = b; out[6] = a / out[0]; out[0] = b; }  // beta
+    else if (op == 3) { out[0] = b; }                                        // first zr
+  }
+}
+
+__global__ void k_sub_scalar(double *__restrict__ v, long long N, const double *__restrict__ c) {
+  const double s = *c;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    v[g] -= s;
+}
+
+__global__ void k_copy(double *__restrict__ d, const double *__restrict__ s, long long N) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    d[g] = s ? s[g] : 0.0;
+}
+
+__global__ void k_cg_update(double *__restrict__ u, double *__restrict__ r, double *__restrict__ rold,
+                            const double *__restrict__ p, const double *__restrict__ q, long long N,
+                            double *__restrict__ part, const double *__restrict__ scal) {
+  const double alpha = scal[5];
+  double a = 0;
+  for (long long g = blockIdx.x * (long long)RB + threadIdx.x; g < N; g += (long long)gridDim.x * RB) {
+    u[g] += alpha * p[g];
+    const double ro = r[g];
+    rold[g] = ro;
+    const double rn = ro - alpha * q[g];
+    r[g] = rn;
+    a += rn * rn;
+  }
+  a = block_sum(a);
+  if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+__global__ void k_p_update(double *__restrict__ p, const double *__restrict__ z, long long N,
+                           const double *__restrict__ scal) {
+  const double beta = scal[6];
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    p[g] = z[g] + beta * p[g];
+}
+
+// b = M * amp * sin(kx x) sin(ky y) sin(kz z) at the nodes (diagonal quadrature)
+__global__ void k_rhs_sin(LevelDev L, double dx, double dy, double dz, double amp, double kx,
+                          double ky, double kz, double *__restrict__ b) {
+  const int n = L.n, n3 = n * n * n;
+  const long long N = (long long)L.Ne * n3;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long e = g / n3;
+    const int t = g - e * n3;
+    const int i = t % n, j = (t / n) % n, k = t / (n * n);
+    const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / ((long long)L.nx * L.ny);
+    const double x = (ex + 0.5 * (L.nodes[i] + 1.0)) * dx;
+    const double y = (ey + 0.5 * (L.nodes[j] + 1.0)) * dy;
+    const double z = (ez + 0.5 * (L.nodes[k] + 1.0)) * dz;
+    b[g] = L.mass[0][i] * L.mass[1][j] * L.mass[2][k] * amp * sin(kx * x) * sin(ky * y) * sin(kz * z);
+  }
+}
+
+
+}  // namespace
+
+cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
+                        cudaStream_t s) {
+  const int z = zero ? 1 : 0;
+  const size_t sb = T ? sizeof(double) * ((size_t)L.n * L.n * L.n + 12 * L.n) : 0;
+  if (T && sb > 48 * 1024) {
+    static bool cfg = false;
+    if (!cfg) {
+      cfg = true;
+      cudaFuncSetAttribute(k_fold2<17, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_fold2<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
+  }
+#define PMG_FOLD(NN)                                                                          \
+  if (T) k_fold2<NN, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);                             \
+  else k_fold2<NN, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+  if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
+    if (L.n == 33) k_fold2<33, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else if (L.n == 5) k_fold2<5, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else if (L.n == 3) k_fold2<3, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    else k_fold2<0, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    cudaError_t e0 = cudaGetLastError();
+    if (e0 == cudaSuccess) e0 = launch_traces(L, u, T, s);
+    return e0;
+  }
+  switch (L.n) {
+    case 3: PMG_FOLD(3) break;
+    case 5: PMG_FOLD(5) break;
+    case 9: PMG_FOLD(9) break;
+    case 17: PMG_FOLD(17) break;
+    case 33: PMG_FOLD(33) break;
+    default: PMG_FOLD(0) break;
+  }
+#undef PMG_FOLD
+  cudaError_t e = cudaGetLastError();
+  return e;
+}
+cudaError_t launch_coarse_gather(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                 const double *mean, double *G, cudaStream_t s) {
+  k_coarse_gather<<<grid_for(8LL * L0.Ne, 256), 256, 0, s>>>(L0.nx, L0.ny, L0.nz, f0, mean, G);
+  return cudaGetLastError();
+}
+cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, const double *in,
+                                double *out, cudaStream_t s) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, axis, forward ? 1 : 0, in, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                double *G1, double *G2, double *u0, cudaStream_t s) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  const long long cols = (long long)C.G[0] * C.G[1];
+  k_coarse_xf<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, f0, G1);
+  k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 1, G1, G2);
+  if (C.G[2] > 32) return cudaErrorInvalidValue;
+  k_coarse_z<<<grid_for(cols * 32, 256), 256, 0, s>>>(C, G2);
+  k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 0, G2, G1);
+  k_coarse_xb<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, G1, u0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s) {
+  const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
+  k_coarse_divide<<<grid_for(N, 256), 256, 0, s>>>(C, G);
+  return cudaGetLastError();
+}
+cudaError_t launch_coarse_scatter(const LevelDev &L0, const CoarseDev &C, const double *G,
+                                  const double *mean, double *u0, cudaStream_t s) {
+  k_coarse_scatter<<<grid_for(8LL * L0.Ne, 256), 256, 0, s>>>(L0.nx, L0.ny, L0.nz, G, mean, u0);
+  return cudaGetLastError();
+}
+int reduce_blocks(long long N) {
+  long long b = (N + 4 * RB - 1) / (4 * RB);
+  if (b > RMAX) b = RMAX;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+cudaError_t launch_sum(const double *x, long long N, double *partial, double *out, double scale,
+                       cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<0><<<nb, RB, 0, s>>>(x, nullptr, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, out, scale, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot(const double *x, const double *y, long long N, double *partial,
+                       double *out, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<1><<<nb, RB, 0, s>>>(x, y, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, out, 1.0, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_sub_scalar(double *v, long long N, const double *c, cudaStream_t s) {
+  k_sub_scalar<<<grid_for(N, 256), 256, 0, s>>>(v, N, c);
+  return cudaGetLastError();
+}
+cudaError_t launch_copy(double *dst, const double *src, long long N, cudaStream_t s) {
+  k_copy<<<grid_for(N, 256), 256, 0, s>>>(dst, src, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_zero(double *dst, long long N, cudaStream_t s) { return launch_copy(dst, nullptr, N, s); }
+cudaError_t launch_pq_alpha(const double *p, const double *q, long long N, double *partial,
+                            double *scal, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<1><<<nb, RB, 0, s>>>(p, q, nullptr, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, scal, 1.0, 1);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update(double *u, double *r, double *rold, const double *p,
+                             const double *q, long long N, double *partial, double *scal,
+                             cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_cg_update<<<nb, RB, 0, s>>>(u, r, rold, p, q, N, partial, scal);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 1, scal + 2, 1.0, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_zr_beta(const double *z, const double *r, const double *rold, long long N,
+                           double *partial, double *scal, bool first, cudaStream_t s) {
+  const int nb = reduce_blocks(N);
+  k_partial<2><<<nb, RB, 0, s>>>(z, r, rold, N, partial);
+  k_final<<<1, RB, 0, s>>>(partial, nb, 2, scal, 1.0, first ? 3 : 2);
+  return cudaGetLastError();
+}
+cudaError_t launch_p_update(double *p, const double *z, long long N, const double *scal,
+                            cudaStream_t s) {
+  k_p_update<<<grid_for(N, 256), 256, 0, s>>>(p, z, N, scal);
+  return cudaGetLastError();
+}
+cudaError_t launch_rhs_sin(const LevelDev &L, double dx, double dy, double dz, double amp,
+                           double kx, double ky, double kz, double *b, cudaStream_t s) {
+  k_rhs_sin<<<grid_for((long long)L.Ne * L.n * L.n * L.n, 256), 256, 0, s>>>(L, dx, dy, dz, amp,
+                                                                             kx, ky, kz, b);
+  return cudaGetLastError();
+}
+
+}  // namespace pmg

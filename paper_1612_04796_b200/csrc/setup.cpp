@@ -252,13 +252,10 @@ std::vector<ld> hat_weights(const Basis1D &b, const Overlap1D &ov) {
   return w;
 }
 
-void gen_eig(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vector<ld> &lam,
-             std::vector<ld> &S) {
-  std::vector<ld> A(m * m), V(m * m, 0), isq(m);
-  for (int i = 0; i < m; ++i) isq[i] = 1 / std::sqrt(M[i]);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j)
-      A[i * m + j] = isq[i] * (L[i * m + j] + L[j * m + i]) / 2 * isq[j];
+// cyclic Jacobi on the symmetric m x m matrix A (row-major, destroyed: its diagonal ends up
+// holding the eigenvalues); V receives the orthonormal eigenvectors as columns
+static void jacobi(int m, std::vector<ld> &A, std::vector<ld> &V) {
+  V.assign(size_t(m) * m, 0);
   for (int i = 0; i < m; ++i) V[i * m + i] = 1;
   ld norm = 0;
   for (int i = 0; i < m * m; ++i) norm += A[i] * A[i];
@@ -291,20 +288,103 @@ void gen_eig(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vec
         }
       }
   }
-  std::vector<int> ord(m);
-  for (int i = 0; i < m; ++i) ord[i] = i;
-  std::sort(ord.begin(), ord.end(), [&](int x, int y) { return A[x * m + x] < A[y * m + y]; });
-  lam.assign(m, 0); S.assign(m * m, 0);
-  for (int i = 0; i < m; ++i) {
-    int c = ord[i];
-    lam[i] = A[c * m + c];
-    // fix the sign: largest-magnitude component positive (deterministic)
+}
+
+// append the eigenpairs of block B (size mb; vectors expanded to length m by `expand`) to
+// (lam, S) in ascending eigenvalue order; sign fixed: largest-magnitude component positive
+template <class Expand>
+static void append_modes(int m, int mb, std::vector<ld> &Bm, const std::vector<ld> &isq,
+                         Expand expand, std::vector<ld> &lam, std::vector<std::vector<ld>> &cols) {
+  std::vector<ld> V;
+  jacobi(mb, Bm, V);
+  std::vector<int> ord(mb);
+  for (int i = 0; i < mb; ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](int x, int y) { return Bm[x * mb + x] < Bm[y * mb + y]; });
+  for (int i = 0; i < mb; ++i) {
+    const int c = ord[i];
+    std::vector<ld> v(m);
+    expand(V, mb, c, v);
     int amax = 0;
     for (int a = 1; a < m; ++a)
-      if (std::fabs(V[a * m + c]) > std::fabs(V[amax * m + c])) amax = a;
-    ld sg = V[amax * m + c] < 0 ? -1 : 1;
-    for (int a = 0; a < m; ++a) S[a * m + i] = sg * isq[a] * V[a * m + c];
+      if (std::fabs(v[a]) > std::fabs(v[amax])) amax = a;
+    const ld sg = v[amax] < 0 ? -1 : 1;
+    for (int a = 0; a < m; ++a) v[a] = sg * isq[a] * v[a];
+    lam.push_back(Bm[c * mb + c]);
+    cols.push_back(v);
   }
+}
+
+void gen_eig(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vector<ld> &lam,
+             std::vector<ld> &S) {
+  std::vector<ld> A(m * m), isq(m);
+  for (int i = 0; i < m; ++i) isq[i] = 1 / std::sqrt(M[i]);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j)
+      A[i * m + j] = isq[i] * (L[i * m + j] + L[j * m + i]) / 2 * isq[j];
+  std::vector<std::vector<ld>> cols;
+  lam.clear();
+  append_modes(m, m, A, isq,
+               [](const std::vector<ld> &V, int mb, int c, std::vector<ld> &v) {
+                 for (int a = 0; a < mb; ++a) v[a] = V[a * mb + c];
+               },
+               lam, cols);
+  S.assign(size_t(m) * m, 0);
+  for (int i = 0; i < m; ++i)
+    for (int a = 0; a < m; ++a) S[a * m + i] = cols[i][a];
+}
+
+// Reflection-symmetric window (odd m = 2H + 1; uniform grid: n_L = n_R):
+// L_s and M_s commute with the reflection a -> m-1-a, so the generalized eigenproblem splits
+// into an even block (H + 1 modes) and an odd block (H modes).  Solving the two blocks
+// separately gives eigenvectors of EXACT parity (S[m-1-a][i] = +-S[a][i] bit for bit), which
+// the even/odd fast-diagonalisation kernels rely on.  Column order: even modes ascending, then
+// odd modes ascending (lam in the same order).
+void gen_eig_parity(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vector<ld> &lam,
+                    std::vector<ld> &S) {
+  const int H = m / 2;
+  std::vector<ld> Ms(m), isq(m), A(size_t(m) * m);
+  for (int a = 0; a < m; ++a) Ms[a] = (M[a] + M[m - 1 - a]) / 2;
+  for (int a = 0; a < m; ++a) isq[a] = 1 / std::sqrt(Ms[a]);
+  for (int a = 0; a < m; ++a)
+    for (int b = 0; b < m; ++b) {
+      const ld l1 = (L[a * m + b] + L[b * m + a]) / 2;
+      const ld l2 = (L[(m - 1 - a) * m + (m - 1 - b)] + L[(m - 1 - b) * m + (m - 1 - a)]) / 2;
+      A[a * m + b] = isq[a] * ((l1 + l2) / 2) * isq[b];
+    }
+  const ld r2 = std::sqrt(ld(2));
+  // even block: basis (e_a + e_{m-1-a}) / sqrt2 (a < H), e_H
+  std::vector<ld> E(size_t(H + 1) * (H + 1)), O(size_t(H) * H);
+  for (int i = 0; i <= H; ++i)
+    for (int j = 0; j <= H; ++j) {
+      ld v;
+      if (i < H && j < H) v = A[i * m + j] + A[i * m + (m - 1 - j)];
+      else if (i < H) v = r2 * A[i * m + H];
+      else if (j < H) v = r2 * A[H * m + j];
+      else v = A[H * m + H];
+      E[i * (H + 1) + j] = v;
+    }
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < H; ++j) O[i * H + j] = A[i * m + j] - A[i * m + (m - 1 - j)];
+  std::vector<std::vector<ld>> cols;
+  lam.clear();
+  append_modes(m, H + 1, E, isq,
+               [m, H, r2](const std::vector<ld> &V, int mb, int c, std::vector<ld> &v) {
+                 for (int a = 0; a < H; ++a) v[a] = v[m - 1 - a] = V[a * mb + c] / r2;
+                 v[H] = V[H * mb + c];
+               },
+               lam, cols);
+  append_modes(m, H, O, isq,
+               [m, H, r2](const std::vector<ld> &V, int mb, int c, std::vector<ld> &v) {
+                 for (int a = 0; a < H; ++a) {
+                   v[a] = V[a * mb + c] / r2;
+                   v[m - 1 - a] = -v[a];
+                 }
+                 v[H] = 0;
+               },
+               lam, cols);
+  S.assign(size_t(m) * m, 0);
+  for (int i = 0; i < m; ++i)
+    for (int a = 0; a < m; ++a) S[a * m + i] = cols[i][a];
 }
 
 }  // namespace pmg

@@ -48,5 +48,8 @@ std::vector<ld> hat_weights(const Basis1D &b, const Overlap1D &ov);
 // S[a*m + i] = component a of eigenvector i.
 void gen_eig(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vector<ld> &lam,
              std::vector<ld> &S);
+// exact-parity variant for reflection-symmetric odd windows: even modes, then odd modes
+void gen_eig_parity(int m, const std::vector<ld> &L, const std::vector<ld> &M, std::vector<ld> &lam,
+                    std::vector<ld> &S);
 
 }  // namespace pmg

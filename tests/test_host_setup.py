@@ -65,7 +65,13 @@ def test_tables_match_oracle(name):
                 m = len(win)
                 lam = g.table(l, d, 4)
                 S = g.table(l, d, 3).reshape(m, m)
-                assert np.allclose(lam, lam_o, rtol=1e-13, atol=0)
+                # modes come as [even ascending, odd ascending] (exact-parity eigensolver)
+                assert np.allclose(np.sort(lam), np.sort(lam_o), rtol=1e-13, atol=0)
+                H = m // 2
+                R = S[::-1, :]                      # reflection a -> m-1-a
+                assert np.array_equal(R[:, :H + 1], S[:, :H + 1])      # even modes, bit-exact
+                assert np.array_equal(R[:, H + 1:], -S[:, H + 1:])     # odd modes, bit-exact
+                assert np.all(np.diff(lam[:H + 1]) >= 0) and np.all(np.diff(lam[H + 1:]) >= 0)
                 # sign-invariant comparison: the inverse S Lambda^-1 S^T
                 inv = (S / lam) @ S.T
                 inv_o = (S_o / lam_o) @ S_o.T
