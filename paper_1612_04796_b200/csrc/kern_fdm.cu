@@ -108,16 +108,23 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : FDM_BIG_THREADS, KSMAX <= 4
 // with S_E = S[0..H][0..H], S_O = S[0..H-1][H+1..2H].  The same number of shared-memory loads
 // feed 2 x MT x KS DMMAs per 8-column tile instead of ceil(m/8) x ceil(m/4) (23: 12 vs 18,
 // 27: 16 vs 28, 13: 4 vs 8).  Intermediate mode-space data sits along DIR as [t_E ; t_O].
-template <int DIR, int MT, int KS, bool FWD, class Epi>
+// QF: tile columns enumerate the Q direction fastest.  With the plane stride padded to 4 mod 16
+// doubles (eo_plane_stride), the B-fragment loads of the x and y passes (QF) and of the z pass
+// (!QF) hit 16 distinct 8-byte bank pairs per half warp.  Software pipelined: the loads and
+// DMMAs of tile i+1 are issued before the epilogue of tile i (ping-pong accumulators).
+template <int DIR, int MT, int KS, bool FWD, bool QF, class Epi>
 __device__ __forceinline__ void eo_lines(const double *X, const Blk &B, const double *S, Epi &epi) {
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
   const int m = B.m[DIR], H = m >> 1;
   const int mp = B.m[PD], mq = B.m[QD];
   const int ncol = mp * mq;
-  const unsigned magic = 0xFFFFFFFFu / (unsigned)mp + 1u;
+  const int mf = QF ? mq : mp;
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)mf + 1u;
   const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int ntiles = (ncol + 7) >> 3;
+  if (warp >= ntiles) return;
   double aE[MT][KS], aO[MT][KS];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt)
@@ -140,17 +147,19 @@ __device__ __forceinline__ void eo_lines(const double *X, const Blk &B, const do
     if (FWD) {                                    // lo = x_k, hi = x_{m-1-k}
       const int kl = min(k, H);
       off1[ks] = kl * so; off2[ks] = (m - 1 - kl) * so;
-      f1[ks] = k <= H;                             // even input valid (k == H: x_H alone)
-      f2[ks] = k < H;                              // pair (sum/diff) valid
     } else {                                      // t_E[k], t_O[k]
       off1[ks] = min(k, H) * so; off2[ks] = (H + 1 + min(k, max(H - 1, 0))) * so;
-      f1[ks] = k <= H; f2[ks] = k < H;
     }
+    f1[ks] = k <= H;                              // FWD: even input valid (k == H: x_H alone)
+    f2[ks] = k < H;                               // FWD: pair valid; BWD: odd mode valid
   }
-  const int ntiles = (ncol + 7) >> 3;
-  for (int tile = warp; tile < ntiles; tile += nw) {
-    const int nb = min(tile * 8 + g, ncol - 1);
-    const int qb = __umulhi((unsigned)nb, magic), pb = nb - qb * mp;
+  auto colpq = [&](int n, int &p, int &q) {
+    const int sl = __umulhi((unsigned)n, magic), f = n - sl * mf;
+    if (QF) { q = f; p = sl; } else { p = f; q = sl; }
+  };
+  auto compute = [&](int tile, double (&cE)[MT][2], double (&cO)[MT][2]) {
+    int pb, qb;
+    colpq(min(tile * 8 + g, ncol - 1), pb, qb);
     const double *xb = X + pb * sp + qb * sq;
     double bE[KS], bO[KS];
 #pragma unroll
@@ -164,7 +173,6 @@ __device__ __forceinline__ void eo_lines(const double *X, const Blk &B, const do
         bO[ks] = f2[ks] ? v2 : 0.0;
       }
     }
-    double cE[MT][2], cO[MT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) { cE[mt][0] = cE[mt][1] = cO[mt][0] = cO[mt][1] = 0.0; }
 #pragma unroll
@@ -174,12 +182,14 @@ __device__ __forceinline__ void eo_lines(const double *X, const Blk &B, const do
         dmma884(cE[mt][0], cE[mt][1], aE[mt][ks], bE[ks]);
         dmma884(cO[mt][0], cO[mt][1], aO[mt][ks], bO[ks]);
       }
-    __syncwarp();
+  };
+  auto epilogue = [&](int tile, const double (&cE)[MT][2], const double (&cO)[MT][2]) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int n = tile * 8 + 2 * t + j;
       if (n >= ncol) continue;
-      const int q = __umulhi((unsigned)n, magic), p = n - q * mp;
+      int p, q;
+      colpq(n, p, q);
       const double cf = epi.template col<DIR>(p, q);
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -197,6 +207,22 @@ __device__ __forceinline__ void eo_lines(const double *X, const Blk &B, const do
         }
       }
     }
+  };
+  double cE0[MT][2], cO0[MT][2], cE1[MT][2], cO1[MT][2];
+  int tile = warp;
+  compute(tile, cE0, cO0);
+  for (;;) {
+    const int t1 = tile + nw;
+    if (t1 < ntiles) compute(t1, cE1, cO1);
+    __syncwarp();
+    epilogue(tile, cE0, cO0);
+    if (t1 >= ntiles) break;
+    const int t2 = t1 + nw;
+    if (t2 < ntiles) compute(t2, cE0, cO0);
+    __syncwarp();
+    epilogue(t1, cE1, cO1);
+    if (t2 >= ntiles) break;
+    tile = t2;
   }
 }
 
@@ -319,10 +345,34 @@ __host__ __device__ __forceinline__ int eo_variant(int m) {
 template <int DIR, int VMAX, bool FWD, class Epi>
 __device__ __forceinline__ void eo_dispatch(const double *X, const Blk &B, const double *S, Epi &epi) {
   const int v = eo_variant(B.m[DIR]);
-  if (v == 1) eo_lines<DIR, 1, 1, FWD>(X, B, S, epi);
-  else if (VMAX >= 2 && v == 2) eo_lines<DIR, 1, 2, FWD>(X, B, S, epi);
-  else if (VMAX >= 3 && v == 3) eo_lines<DIR, 2, 3, FWD>(X, B, S, epi);
-  else if (VMAX >= 4) eo_lines<DIR, 2, 4, FWD>(X, B, S, epi);
+  constexpr bool QF = DIR != 2;                  // x, y passes: z-fastest columns
+  if (v == 1) eo_lines<DIR, 1, 1, FWD, QF>(X, B, S, epi);
+  else if (VMAX >= 2 && v == 2) eo_lines<DIR, 1, 2, FWD, QF>(X, B, S, epi);
+  else if (VMAX >= 3 && v == 3) eo_lines<DIR, 2, 3, FWD, QF>(X, B, S, epi);
+  else if (VMAX >= 4) eo_lines<DIR, 2, 4, FWD, QF>(X, B, S, epi);
+}
+
+// shared-memory plane stride of the window: m0*m1 padded to 4 mod 16 doubles (bank spread)
+__host__ __device__ __forceinline__ int eo_plane_stride(int m0, int m1) {
+  const int a = m0 * m1;
+  return a + ((4 - (a & 15)) & 15);
+}
+
+// gather into the padded window layout X[a + m0 b + s2 c]; one warp per window row (m0 <= 32)
+__device__ __forceinline__ void eo_gather(const LevelDev &L, const double *r, const long long *offs,
+                                          double *X, int s2) {
+  const int m0 = L.m[0], m1 = L.m[1], m2 = L.m[2];
+  const long long *xo = offs, *yo = offs + m0, *zo = offs + m0 + m1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const long long xa = lane < m0 ? xo[lane] : 0;
+  const int rows = m1 * m2;
+  int b = warp % m1, c = warp / m1;
+  const int db = nw % m1, dc = nw / m1;
+  for (int row = warp; row < rows; row += nw) {
+    if (lane < m0) cp_async8(X + lane + m0 * b + s2 * c, r + xa + yo[b] + zo[c]);
+    b += db; c += dc;
+    if (b >= m1) { b -= m1; ++c; }
+  }
 }
 
 template <int VMAX>
@@ -344,10 +394,11 @@ __global__ void __launch_bounds__(VMAX <= 2 ? 128 : 256, VMAX <= 2 ? 8 : 2) k_fd
   extern __shared__ double sm[];
   const int m[3] = {L.m[0], L.m[1], L.m[2]};
   const int Mw = L.Mw;
+  const int s2 = eo_plane_stride(m[0], m[1]);
   double *X = sm;
   double *Ss[3];
   double *lam[3], *W[3];
-  double *p = sm + Mw;
+  double *p = sm + s2 * m[2];
   for (int d = 0; d < 3; ++d) { Ss[d] = p; p += m[d] * m[d]; }
   for (int d = 0; d < 3; ++d) { lam[d] = p; p += m[d]; }
   for (int d = 0; d < 3; ++d) { W[d] = p; p += m[d]; }
@@ -365,10 +416,11 @@ __global__ void __launch_bounds__(VMAX <= 2 ? 128 : 256, VMAX <= 2 ? 8 : 2) k_fd
   }
   fdm_offsets(L, e, offs);
   __syncthreads();
-  fdm_gather(L, r, offs, X);
+  eo_gather(L, r, offs, X, s2);
   cp_async_wait_all();
   __syncthreads();
-  const Blk B = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};
+  const Blk B = {{m[0], m[1], m[2]}, {1, m[0], s2}};
+  const Blk G = {{m[0], m[1], m[2]}, {1, m[0], m[0] * m[1]}};   // global window order (Z)
   const double *lamc[3] = {lam[0], lam[1], lam[2]};
   EpiStore st{X, B};
   eo_dispatch<0, VMAX, true>(X, B, Ss[0], st); __syncthreads();
@@ -379,7 +431,7 @@ __global__ void __launch_bounds__(VMAX <= 2 ? 128 : 256, VMAX <= 2 ? 8 : 2) k_fd
     EpiWeightRed wr{u, offs, m[0], m[1], {W[0], W[1], W[2]}};
     eo_dispatch<0, VMAX, false>(X, B, Ss[0], wr);
   } else {
-    EpiWeightStore ws{Z + (long long)e * Mw, B, {W[0], W[1], W[2]}};
+    EpiWeightStore ws{Z + (long long)e * Mw, G, {W[0], W[1], W[2]}};
     eo_dispatch<0, VMAX, false>(X, B, Ss[0], ws);
   }
 }
@@ -400,12 +452,19 @@ static void configure_smem() {
   cudaFuncSetAttribute(k_fdm_eo<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 
+static size_t fdm_eo_smem_bytes(const LevelDev &L) {
+  size_t d = (size_t)eo_plane_stride(L.m[0], L.m[1]) * L.m[2];
+  for (int k = 0; k < 3; ++k) d += (size_t)L.m[k] * L.m[k] + 3 * (size_t)L.m[k];   // S, lam, W, offsets
+  return d * sizeof(double);
+}
+
 // even/odd kernels need odd windows (reflection symmetric; always the case for n = 2^l + 1)
 static bool fdm_eo_ok(const LevelDev &L) {
 #ifdef PMG_NO_EO
   return false;
 #endif
-  return (L.m[0] & 1) && (L.m[1] & 1) && (L.m[2] & 1);
+  return (L.m[0] & 1) && (L.m[1] & 1) && (L.m[2] & 1) && L.m[0] <= 32 && L.m[1] <= 32 &&
+         L.m[2] <= 32 && fdm_eo_smem_bytes(L) <= 227 * 1024;
 }
 
 static int fdm_eo_vmax(const LevelDev &L) {
@@ -445,9 +504,13 @@ cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cu
   const size_t sb = fdm_mma_smem_bytes(L);
   const int ks = (std::max(L.m[0], std::max(L.m[1], L.m[2])) + 3) >> 2;
   const int grid = L.Ne / 8;
+  if (fdm_eoc_launch(L, r, nullptr, 0, u, s)) {
+    for (int color = 1; color < 8; ++color) fdm_eoc_launch(L, r, nullptr, color, u, s);
+    return cudaGetLastError();
+  }
   if (fdm_eo_ok(L)) {
     for (int color = 0; color < 8; ++color)
-      fdm_eo_launch(L, grid, sb, s, [&](auto kern, int gr, int th, size_t b, cudaStream_t st) {
+      fdm_eo_launch(L, grid, fdm_eo_smem_bytes(L), s, [&](auto kern, int gr, int th, size_t b, cudaStream_t st) {
         kern<<<gr, th, b, st>>>(L, r, nullptr, color, u);
       });
     return cudaGetLastError();
@@ -462,11 +525,12 @@ cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cu
 
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s) {
+  if (fdm_eoc_launch(L, r, Z, -1, nullptr, s)) return cudaGetLastError();   // compile-time shape
   if (fdm_mma_ok(L)) {
     configure_smem();
     const size_t sb = fdm_mma_smem_bytes(L);
     if (fdm_eo_ok(L)) {
-      fdm_eo_launch(L, L.Ne, sb, s, [&](auto kern, int gr, int th, size_t b, cudaStream_t st) {
+      fdm_eo_launch(L, L.Ne, fdm_eo_smem_bytes(L), s, [&](auto kern, int gr, int th, size_t b, cudaStream_t st) {
         kern<<<gr, th, b, st>>>(L, r, Z, -1, nullptr);
       });
       return cudaGetLastError();

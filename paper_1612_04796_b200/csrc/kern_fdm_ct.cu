@@ -1,0 +1,339 @@
+// Schwarz subdomain solves (fast diagonalisation, even/odd split) specialised at compile time
+// for the window shapes of the benchmark configurations.  arXiv:1612.04796
+// (Eq. 9 subdomain problem, the fast-diagonalisation formula, Eq. 10 weighted scatter).
+//
+// Same method as k_fdm_eo in kern_fdm.cu (see the comment there for the even/odd algebra); with
+// every extent and stride a compile-time constant the tile loops carry no runtime index
+// arithmetic beyond the lane's own column, the A fragments stay in registers for a whole pass,
+// and the B fragments need no selects:
+//   forward:  b_E = x_k + x_{m-1-k}, b_O = x_k - x_{m-1-k} with k clamped to H; the middle
+//             column of S_E^T is halved (x_H + x_H = 2 x_H exactly), padding columns are zero;
+//   backward: b_E = t_E[min(k, H)], b_O = t_O[min(k, H-1)] against zero-padded S_E, S_O.
+#include <algorithm>
+
+#include "kcommon.cuh"
+
+namespace pmg {
+namespace {
+
+__host__ __device__ constexpr int plane_stride(int m0, int m1) {
+  return m0 * m1 + ((4 - ((m0 * m1) & 15)) & 15);   // 4 mod 16 doubles: bank spread
+}
+
+template <int M0, int M1, int M2>
+struct Shape {
+  static constexpr int S2 = plane_stride(M0, M1);
+  static constexpr int Hmax = (M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2)) / 2;
+  static constexpr int THREADS = Hmax >= 8 ? 256 : 128;
+  static constexpr int MINB = Hmax >= 8 ? 2 : 8;
+  template <int D> __host__ __device__ static constexpr int m() { return D == 0 ? M0 : (D == 1 ? M1 : M2); }
+  template <int D> __host__ __device__ static constexpr int s() { return D == 0 ? 1 : (D == 1 ? M0 : S2); }
+};
+
+template <int DIR, class SH, bool FWD, bool QF, class Epi>
+__device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi &epi) {
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  constexpr int m = SH::template m<DIR>(), H = m / 2;
+  constexpr int MT = (H + 1 + 7) / 8, KS = (H + 1 + 3) / 4;
+  constexpr int MP = SH::template m<PD>(), MQ = SH::template m<QD>();
+  constexpr int SO = SH::template s<DIR>(), SP = SH::template s<PD>(), SQ = SH::template s<QD>();
+  constexpr int NCOL = MP * MQ, NT = (NCOL + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = SH::THREADS / 32;
+  const int g = lane >> 2, t = lane & 3;
+  if (warp >= NT) return;
+  double aE[MT][KS], aO[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      if (FWD) {
+        aE[mt][ks] = (o <= H && k <= H) ? S[k * m + o] * (k == H ? 0.5 : 1.0) : 0.0;
+        aO[mt][ks] = (o < H && k < H) ? S[k * m + H + 1 + o] : 0.0;
+      } else {
+        aE[mt][ks] = (o <= H && k <= H) ? S[o * m + k] : 0.0;
+        aO[mt][ks] = (o < H && k < H) ? S[o * m + H + 1 + k] : 0.0;
+      }
+    }
+  int off1[KS], off2[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + t;
+    if (FWD) {
+      const int kl = min(k, H);
+      off1[ks] = kl * SO; off2[ks] = (m - 1 - kl) * SO;
+    } else {
+      off1[ks] = min(k, H) * SO; off2[ks] = (H + 1 + min(k, H - 1)) * SO;
+    }
+  }
+  auto colpq = [](int n, int &p, int &q) {
+    if (QF) { p = n / MQ; q = n - p * MQ; } else { q = n / MP; p = n - q * MP; }
+  };
+  auto compute = [&](int tile, double (&cE)[MT][2], double (&cO)[MT][2]) {
+    int pb, qb;
+    colpq(min(tile * 8 + g, NCOL - 1), pb, qb);
+    const double *xb = X + pb * SP + qb * SQ;
+    double bE[KS], bO[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double v1 = xb[off1[ks]], v2 = xb[off2[ks]];
+      if (FWD) { bE[ks] = v1 + v2; bO[ks] = v1 - v2; }
+      else { bE[ks] = v1; bO[ks] = v2; }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { cE[mt][0] = cE[mt][1] = cO[mt][0] = cO[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        dmma884(cE[mt][0], cE[mt][1], aE[mt][ks], bE[ks]);
+        dmma884(cO[mt][0], cO[mt][1], aO[mt][ks], bO[ks]);
+      }
+  };
+  auto epilogue = [&](int tile, const double (&cE)[MT][2], const double (&cO)[MT][2]) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tile * 8 + 2 * t + j;
+      if (n >= NCOL) continue;
+      int p, q;
+      colpq(n, p, q);
+      const double cf = epi.template col<DIR>(p, q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (FWD) {
+          if (o <= H) epi.template put<DIR>(o, p, q, cf, cE[mt][j]);
+          if (o < H) epi.template put<DIR>(H + 1 + o, p, q, cf, cO[mt][j]);
+        } else if (o < H) {
+          epi.template put<DIR>(o, p, q, cf, cE[mt][j] + cO[mt][j]);
+          epi.template put<DIR>(m - 1 - o, p, q, cf, cE[mt][j] - cO[mt][j]);
+        } else if (o == H) {
+          epi.template put<DIR>(o, p, q, cf, cE[mt][j]);
+        }
+      }
+    }
+  };
+  double cE0[MT][2], cO0[MT][2], cE1[MT][2], cO1[MT][2];
+  int tile = warp;
+  compute(tile, cE0, cO0);
+  for (;;) {
+    const int t1 = tile + NW;
+    if (t1 < NT) compute(t1, cE1, cO1);
+    __syncwarp();
+    epilogue(tile, cE0, cO0);
+    if (t1 >= NT) break;
+    const int t2 = t1 + NW;
+    if (t2 < NT) compute(t2, cE0, cO0);
+    __syncwarp();
+    epilogue(t1, cE1, cO1);
+    if (t2 >= NT) break;
+    tile = t2;
+  }
+}
+
+// z passes fused: forward S_z^T, eigen-divide, backward S_z on warp-private z columns
+template <class SH>
+__device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const double *const *lam) {
+  constexpr int m = SH::template m<2>(), H = m / 2;
+  constexpr int MT = (H + 1 + 7) / 8, KS = (H + 1 + 3) / 4;
+  constexpr int MP = SH::template m<0>(), MQ = SH::template m<1>();
+  constexpr int SO = SH::S2, SQ = SH::template s<1>();
+  constexpr int NCOL = MP * MQ, NT = (NCOL + 7) / 8, NW = SH::THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double aEf[MT][KS], aOf[MT][KS], aEb[MT][KS], aOb[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      const bool e_ok = o <= H && k <= H, o_ok = o < H && k < H;
+      aEf[mt][ks] = e_ok ? S[k * m + o] * (k == H ? 0.5 : 1.0) : 0.0;
+      aOf[mt][ks] = o_ok ? S[k * m + H + 1 + o] : 0.0;
+      aEb[mt][ks] = e_ok ? S[o * m + k] : 0.0;
+      aOb[mt][ks] = o_ok ? S[o * m + H + 1 + k] : 0.0;
+    }
+  int lo[KS], hi[KS], oo[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + t, kl = min(k, H);
+    lo[ks] = kl * SO; hi[ks] = (m - 1 - kl) * SO;
+    oo[ks] = (H + 1 + min(k, H - 1)) * SO;
+  }
+  double lz[MT], lzo[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int o = mt * 8 + g;
+    lz[mt] = lam[2][min(o, H)];
+    lzo[mt] = lam[2][H + 1 + min(o, H - 1)];
+  }
+  for (int tile = warp; tile < NT; tile += NW) {
+    const int nb = min(tile * 8 + g, NCOL - 1);
+    const int qb = nb / MP, pb = nb - qb * MP;
+    double *xb = X + pb + qb * SQ;
+    double bE[KS], bO[KS], cE[MT][2], cO[MT][2];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double v1 = xb[lo[ks]], v2 = xb[hi[ks]];
+      bE[ks] = v1 + v2; bO[ks] = v1 - v2;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { cE[mt][0] = cE[mt][1] = cO[mt][0] = cO[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        dmma884(cE[mt][0], cE[mt][1], aEf[mt][ks], bE[ks]);
+        dmma884(cO[mt][0], cO[mt][1], aOf[mt][ks], bO[ks]);
+      }
+    __syncwarp();
+    int wb[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tile * 8 + 2 * t + j;
+      wb[j] = -1;
+      if (n >= NCOL) continue;
+      const int q = n / MP, p = n - q * MP;
+      wb[j] = p + q * SQ;
+      const double cf = lam[0][p] + lam[1][q];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o <= H) X[wb[j] + o * SO] = cE[mt][j] * rcp_nr(cf + lz[mt]);
+        if (o < H) X[wb[j] + (H + 1 + o) * SO] = cO[mt][j] * rcp_nr(cf + lzo[mt]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      bE[ks] = xb[lo[ks]];                        // t_E[min(k, H)]
+      bO[ks] = xb[oo[ks]];                        // t_O[min(k, H-1)]
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { cE[mt][0] = cE[mt][1] = cO[mt][0] = cO[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        dmma884(cE[mt][0], cE[mt][1], aEb[mt][ks], bE[ks]);
+        dmma884(cO[mt][0], cO[mt][1], aOb[mt][ks], bO[ks]);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (wb[j] < 0) continue;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (o < H) {
+          X[wb[j] + o * SO] = cE[mt][j] + cO[mt][j];
+          X[wb[j] + (m - 1 - o) * SO] = cE[mt][j] - cO[mt][j];
+        } else if (o == H) {
+          X[wb[j] + o * SO] = cE[mt][j];
+        }
+      }
+    }
+  }
+}
+
+// Shared memory: window X (S2 * M2, padded planes) | S_x, S_y, S_z | lam | W | gather offsets
+template <int M0, int M1, int M2>
+__global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>::MINB)
+    k_fdm_eoc(LevelDev L, const double *__restrict__ r, double *__restrict__ Z, int color,
+              double *__restrict__ u) {
+  using SH = Shape<M0, M1, M2>;
+  constexpr int S2 = SH::S2, Mw = M0 * M1 * M2;
+  extern __shared__ double sm[];
+  double *X = sm;
+  double *Ss[3] = {sm + S2 * M2, sm + S2 * M2 + M0 * M0, sm + S2 * M2 + M0 * M0 + M1 * M1};
+  double *lam0 = Ss[2] + M2 * M2;
+  double *lam[3] = {lam0, lam0 + M0, lam0 + M0 + M1};
+  double *W0 = lam0 + M0 + M1 + M2;
+  double *W[3] = {W0, W0 + M0, W0 + M0 + M1};
+  long long *offs = reinterpret_cast<long long *>(W0 + M0 + M1 + M2);
+  constexpr int mm[3] = {M0, M1, M2};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    stage(Ss[d], L.S[d], mm[d] * mm[d]);
+    stage(lam[d], L.lam[d], mm[d]);
+    stage(W[d], L.W[d], mm[d]);
+  }
+  int e = blockIdx.x;
+  if (color >= 0) {       // subdomain bx of parity class `color` (2x2x2 colouring)
+    const int hx = L.nx >> 1, hy = L.ny >> 1;
+    const int bx = e % hx, by = (e / hx) % hy, bz = e / (hx * hy);
+    e = (2 * bx + (color & 1)) + L.nx * ((2 * by + ((color >> 1) & 1)) + L.ny * (2 * bz + (color >> 2)));
+  }
+  fdm_offsets(L, e, offs);
+  __syncthreads();
+  {   // gather: one warp per window row (M0 <= 32), padded plane stride
+    const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = SH::THREADS / 32;
+    const long long xa = lane < M0 ? xo[lane] : 0;
+    for (int row = warp; row < M1 * M2; row += NW) {
+      const int c = row / M1, b = row - c * M1;
+      if (lane < M0) cp_async8(X + lane + M0 * b + S2 * c, r + xa + yo[b] + zo[c]);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const Blk B = {{M0, M1, M2}, {1, M0, S2}};
+  const double *lamc[3] = {lam[0], lam[1], lam[2]};
+  EpiStore st{X, B};
+  eoc_lines<0, SH, true, true>(X, Ss[0], st); __syncthreads();
+  eoc_lines<1, SH, true, true>(X, Ss[1], st); __syncthreads();
+  eoc_z_fused<SH>(X, Ss[2], lamc); __syncthreads();
+  eoc_lines<1, SH, false, true>(X, Ss[1], st); __syncthreads();
+  if (color >= 0) {
+    EpiWeightRed wr{u, offs, M0, M1, {W[0], W[1], W[2]}};
+    eoc_lines<0, SH, false, true>(X, Ss[0], wr);
+  } else {
+    const Blk G = {{M0, M1, M2}, {1, M0, M0 * M1}};   // global window order (Z)
+    EpiWeightStore ws{Z + (long long)e * Mw, G, {W[0], W[1], W[2]}};
+    eoc_lines<0, SH, false, true>(X, Ss[0], ws);
+  }
+}
+
+template <int M0, int M1, int M2>
+size_t eoc_smem() {
+  return sizeof(double) * ((size_t)Shape<M0, M1, M2>::S2 * M2 + M0 * M0 + M1 * M1 + M2 * M2 +
+                           3 * (M0 + M1 + M2));
+}
+
+template <int M0, int M1, int M2>
+void eoc_launch(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
+                cudaStream_t s) {
+  const size_t sb = eoc_smem<M0, M1, M2>();
+  static bool cfg = false;
+  if (!cfg) {
+    cfg = true;
+    cudaFuncSetAttribute(k_fdm_eoc<M0, M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
+  k_fdm_eoc<M0, M1, M2><<<grid, Shape<M0, M1, M2>::THREADS, sb, s>>>(L, r, Z, color, u);
+}
+
+}  // namespace
+
+// Shapes of the benchmark configurations (c1-c5, all levels); others use the generic kernels.
+#define PMG_EOC_SHAPES(X) \
+  X(23, 23, 23) X(13, 13, 13) X(7, 7, 7) X(5, 5, 5) X(11, 27, 27) X(7, 15, 15) X(5, 9, 9)
+
+bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, double *u,
+                    cudaStream_t s) {
+#ifdef PMG_NO_EOC
+  return false;
+#endif
+  const int grid = color >= 0 ? L.Ne / 8 : L.Ne;
+#define PMG_EOC_CASE(a, b, c)                                    \
+  if (L.m[0] == a && L.m[1] == b && L.m[2] == c) {              \
+    eoc_launch<a, b, c>(L, grid, r, Z, color, u, s);            \
+    return true;                                                \
+  }
+  PMG_EOC_SHAPES(PMG_EOC_CASE)
+#undef PMG_EOC_CASE
+  return false;
+}
+
+}  // namespace pmg

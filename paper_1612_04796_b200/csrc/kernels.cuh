@@ -51,6 +51,9 @@ cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cu
 bool prolong_traces_ok(const LevelDev &Lf, int nc);
 cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, const double *uc,
                                   double *uf, double *T, cudaStream_t s);
+// compile-time-shape even/odd Schwarz kernel (kern_fdm_ct.cu); false if the shape is not built in
+bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, double *u,
+                    cudaStream_t s);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
