@@ -124,6 +124,23 @@ def cycle_model(g, c):
     return flops, bytes_, fdm_flops_top
 
 
+def fdm_issued_flops(g, level):
+    """FP64 tensor-core flops the even/odd Schwarz kernel actually issues on `level` (DMMA
+    m8n8k4 = 512 flop): per 8-column tile of a 1D pass along d (extent m = 2H+1) it runs
+    2 x ceil((H+1)/8) x ceil((H+1)/4) DMMAs (even and odd half-GEMMs); six passes (the z pass
+    fused: forward + backward).  The algorithmic count (fdm_flops_top) is the dense one."""
+    n = 2 ** level + 1
+    Ne = g.ndofs(level) // n ** 3
+    _, m = g.level_overlap(level)
+    dm = 0
+    for d in range(3):
+        H = m[d] // 2
+        per_tile = 2 * ((H + 1 + 7) // 8) * ((H + 1 + 3) // 4)
+        cols = (m[0] * m[1] * m[2]) // m[d]
+        dm += 2 * per_tile * ((cols + 7) // 8)          # forward + backward along d
+    return 512.0 * dm * Ne
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -264,10 +281,28 @@ def run_ours(args, rank, world, local_rank):
                               "ms_per_cycle": round(v[0] / max(pcycles, 1), 4)}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     cyc_t_roof = max(flops / (peak_tf * 1e12), bytes_ / 6554.6e9)
+    issued = fdm_issued_flops(g, top) if all(x % 2 for x in g.level_overlap(top)[1]) else None
+    # operator apply / residual on the top level (the three per cycle: two residuals and the
+    # residual fused with the restriction): DOF/s per launch and its HBM roofline (u, f in,
+    # r out = 24 B/DOF, plus the six neighbour-trace segments 6 n^2 x 8 B per element)
+    ap_ms, ap_cnt = prof.get(("apply", top), (0.0, 0))
+    ap_avg_ms = ap_ms / max(ap_cnt, 1)
+    n_top = 2 ** top + 1
+    ap_bytes = N * 24.0 + (N // n_top ** 3) * 6 * n_top ** 2 * 8.0
+    ap_flops = (6 * n_top + (24 if c.basis == 0 else 48)) * N
+    apply_entry = None
+    if ap_avg_ms > 0:
+        t_ap = ap_avg_ms / 1e3
+        apply_entry = {"dof_per_s": N / t_ap, "ms_per_launch": ap_avg_ms, "launches_per_cycle": ap_cnt / max(pcycles, 1),
+                       "bound": "hbm" if ap_bytes / 6554.6e9 > ap_flops / (peak_tf * 1e12) else "alu",
+                       "achieved_gbs": ap_bytes / t_ap / 1e9, "peak_gbs": 6554.6,
+                       "achieved_tflops": ap_flops / t_ap / 1e12,
+                       "frac": max(ap_bytes / 6554.6e9, ap_flops / (peak_tf * 1e12)) / t_ap,
+                       "algorithmic_bytes": ap_bytes, "algorithmic_flops": ap_flops}
     traffic = None      # DRAM bytes per launch of the roofline kernel from the committed ncu capture
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(args.config, {}).get("k_fdm_mma_top")
+        traffic = tr.get(args.config, {}).get("fdm_top")
     except Exception:
         pass
     out = {
@@ -289,7 +324,9 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": (achieved_tf / peak_tf) if achieved_tf else None, "traffic": traffic,
                      "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-                     "kernel": "k_fdm_mma (Schwarz fast-diagonalisation solve, top level)",
+                     "kernel": "k_fdm_eoc (even/odd Schwarz fast-diagonalisation solve, top level); "
+                               "achieved = dense algorithmic flops (SURVEY 8(d), no even/odd savings) / launch time",
+                     "issued_dmma_tflops": (issued / (fdm_avg_ms / 1e3) / 1e12) if (issued and fdm_avg_ms > 0) else None,
                      "kernel_ms_per_launch": fdm_avg_ms,
                      "share_of_step": (fdm_ms / args.steps / ms_profiled) if ms_profiled else None,
                      "peak_source": "measured live by pmg_fp64_peak: max(DFMA %.2f, DMMA %.2f) TFLOP/s; "
@@ -298,6 +335,7 @@ def run_ours(args, rank, world, local_rank):
         "cycle_roofline": {"flop_per_cycle": flops, "bytes_per_cycle": bytes_,
                            "t_roof_ms": cyc_t_roof * 1e3,
                            "frac": cyc_t_roof * 1e3 / (ms_total / max(cycles, 1))},
+        "apply_roofline": apply_entry,
         "residual_reduction_per_cycle": rho,
         "residual_history": hist,
         "kernels": kernels,

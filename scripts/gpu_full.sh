@@ -12,4 +12,4 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fdm_mma|k_apply_mma|k_fold2" -c 3 -o gpurun_out/prof_full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu_full=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fdm_eoc|k_apply_mma|k_fold2" -c 3 -o gpurun_out/prof_full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu_full=$?
