@@ -281,7 +281,8 @@ def run_ours(args, rank, world, local_rank):
                               "ms_per_cycle": round(v[0] / max(pcycles, 1), 4)}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     cyc_t_roof = max(flops / (peak_tf * 1e12), bytes_ / 6554.6e9)
-    issued = fdm_issued_flops(g, top) if all(x % 2 for x in g.level_overlap(top)[1]) else None
+    mt = g.level_overlap(top)[1]
+    issued = fdm_issued_flops(g, top) if (all(x % 2 for x in mt) and max(mt) <= 31) else None   # even/odd kernel only
     # operator apply / residual on the top level (the three per cycle: two residuals and the
     # residual fused with the restriction): DOF/s per launch and its HBM roofline (u, f in,
     # r out = 24 B/DOF, plus the six neighbour-trace segments 6 n^2 x 8 B per element)

@@ -3,7 +3,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpmgdg.so")
+LIB_PATH = os.environ.get("PMG_LIB") or os.path.join(HERE, "libpmgdg.so")   # PMG_LIB: diagnostic builds only
 
 GLL, GL = 0, 1
 OVL_NODES, OVL_REL, OVL_MAXREL = 0, 1, 2

@@ -31,6 +31,7 @@ struct LevelHost {
   // workspace byte offsets
   size_t o_mass[3], o_D[3], o_tr[3], o_S[3], o_lam[3], o_W[3], o_Daug[3], o_interp = 0, o_nodes = 0;
   size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0, o_scr2 = 0, o_cb = 0, o_v = 0;
+  size_t o_x1 = 0, o_x2 = 0;   // transfer scratch (n > 17): Ne * n * n * n_c each
   int fdm_path = 0;          // 0: DMMA in shared memory, 1: global-memory line GEMMs, 2: generic
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
@@ -177,6 +178,11 @@ void plan_workspace(dg_ctx *c) {
     if (n > 17) {                    // global-memory apply buffers (face coefficients, V)
       h.o_cb = p.dbl(Ne * 12 * n * n);
       h.o_v = p.dbl(h.N);
+      if (l >= 1) {
+        const long long nc = c->lev[l - 1].n;
+        h.o_x1 = p.dbl(Ne * n * n * nc);
+        h.o_x2 = p.dbl(Ne * n * n * nc);
+      }
     }
   }
   for (int d = 0; d < 3; ++d) {
@@ -337,8 +343,13 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
                                                        c->lev[l - 1].n, F[l - 1], s));
     } else {
       if ((st = residual_impl(c, l, U[l], F[l], r, s, nu > 0))) return st;    // l.292
-      LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n,
-                                     wsp<double>(c, c->lev[l].o_interp), r, F[l - 1], s));
+      if (c->lev[l].o_x1)
+        LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict_global(d, c->lev[l - 1].n,
+                                       wsp<double>(c, c->lev[l].o_interp), r, F[l - 1],
+                                       wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s));
+      else
+        LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n,
+                                       wsp<double>(c, c->lev[l].o_interp), r, F[l - 1], s));
     }
   }
   if ((st = coarse_impl(c, F[0], U[0], s))) return st;           // l.295
@@ -352,7 +363,11 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
                                                              wsp<double>(c, c->lev[l].o_T), s));
       tr = true;
     } else {
-      LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, nc, Il, U[l - 1], U[l], s));   // l.299
+      if (c->lev[l].o_x1)
+        LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong_global(d, nc, Il, U[l - 1], U[l],
+                                       wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s));
+      else
+        LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, nc, Il, U[l - 1], U[l], s));   // l.299
     }
     if ((st = smooth_impl(c, l, U[l], F[l], c->nu2[l], false, s, false, tr))) return st;  // l.301
   }
@@ -627,8 +642,14 @@ int dg_prolongate_add(dg_ctx *c, int level, const double *uc, double *uf, void *
   if (level < 1 || !uc || !uf) return fail(c, PMG_EINVAL, "dg_prolongate_add: bad arguments");
   pmg::LevelDev d = level_dev(c, level);
   cudaStream_t s = S(stream);
-  LAUNCHK(c, K_PROLONG, level, s, pmg::launch_prolong(d, c->lev[level - 1].n,
-                                wsp<double>(c, c->lev[level].o_interp), uc, uf, s));
+  const LevelHost &h = c->lev[level];
+  if (h.o_x1 && c->ws)
+    LAUNCHK(c, K_PROLONG, level, s, pmg::launch_prolong_global(d, c->lev[level - 1].n,
+                                  wsp<double>(c, h.o_interp), uc, uf, wsp<double>(c, h.o_x1),
+                                  wsp<double>(c, h.o_x2), s));
+  else
+    LAUNCHK(c, K_PROLONG, level, s, pmg::launch_prolong(d, c->lev[level - 1].n,
+                                  wsp<double>(c, h.o_interp), uc, uf, s));
   return PMG_OK;
 }
 
@@ -638,8 +659,14 @@ int dg_restrict(dg_ctx *c, int level, const double *rf, double *fc, void *stream
   if (level < 1 || !rf || !fc) return fail(c, PMG_EINVAL, "dg_restrict: bad arguments");
   pmg::LevelDev d = level_dev(c, level);
   cudaStream_t s = S(stream);
-  LAUNCHK(c, K_RESTRICT, level, s, pmg::launch_restrict(d, c->lev[level - 1].n,
-                                 wsp<double>(c, c->lev[level].o_interp), rf, fc, s));
+  const LevelHost &h = c->lev[level];
+  if (h.o_x1 && c->ws)
+    LAUNCHK(c, K_RESTRICT, level, s, pmg::launch_restrict_global(d, c->lev[level - 1].n,
+                                   wsp<double>(c, h.o_interp), rf, fc, wsp<double>(c, h.o_x1),
+                                   wsp<double>(c, h.o_x2), s));
+  else
+    LAUNCHK(c, K_RESTRICT, level, s, pmg::launch_restrict(d, c->lev[level - 1].n,
+                                   wsp<double>(c, h.o_interp), rf, fc, s));
   return PMG_OK;
 }
 

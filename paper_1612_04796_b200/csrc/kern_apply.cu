@@ -15,7 +15,8 @@ __global__ void k_traces(LevelDev L, const double *__restrict__ u, double *__res
   const int e = blockIdx.x;
   const double *ue = u + (long long)e * n3;
   double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+  // 2D grid: blockIdx.y splits the 3 n^2 face points (large elements fill the GPU)
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < 3 * n2; t += gridDim.y * blockDim.x) {
     const int d = t / n2, p = t - d * n2;
     const int p0 = p % n, p1 = p / n;
     int base, stride;
@@ -277,7 +278,8 @@ cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStr
     }
     k_traces_sm<<<L.Ne, 256, sb, s>>>(L, u, T);
   } else {
-    k_traces<<<L.Ne, 128, 0, s>>>(L, u, T);
+    const int chunks = (3 * n * n + 127) / 128;
+    k_traces<<<dim3(L.Ne, chunks), 128, 0, s>>>(L, u, T);
   }
   return cudaGetLastError();
 }

@@ -265,6 +265,13 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>:
     const int bx = e % hx, by = (e / hx) % hy, bz = e / (hx * hy);
     e = (2 * bx + (color & 1)) + L.nx * ((2 * by + ((color >> 1) & 1)) + L.ny * (2 * bz + (color >> 2)));
   }
+#ifdef PMG_PHASE_TIMING
+  long long tph[8];
+  tph[0] = clock64();
+#define PMG_PH(i) tph[i] = clock64()
+#else
+#define PMG_PH(i)
+#endif
   fdm_offsets(L, e, offs);
   __syncthreads();
   {   // gather: one warp per window row (M0 <= 32), padded plane stride
@@ -279,13 +286,18 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>:
   }
   cp_async_wait_all();
   __syncthreads();
+  PMG_PH(1);
   const Blk B = {{M0, M1, M2}, {1, M0, S2}};
   const double *lamc[3] = {lam[0], lam[1], lam[2]};
   EpiStore st{X, B};
   eoc_lines<0, SH, true, true>(X, Ss[0], st); __syncthreads();
+  PMG_PH(2);
   eoc_lines<1, SH, true, true>(X, Ss[1], st); __syncthreads();
+  PMG_PH(3);
   eoc_z_fused<SH>(X, Ss[2], lamc); __syncthreads();
+  PMG_PH(4);
   eoc_lines<1, SH, false, true>(X, Ss[1], st); __syncthreads();
+  PMG_PH(5);
   if (color >= 0) {
     EpiWeightRed wr{u, offs, M0, M1, {W[0], W[1], W[2]}};
     eoc_lines<0, SH, false, true>(X, Ss[0], wr);
@@ -294,6 +306,15 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>:
     EpiWeightStore ws{Z + (long long)e * Mw, G, {W[0], W[1], W[2]}};
     eoc_lines<0, SH, false, true>(X, Ss[0], ws);
   }
+#ifdef PMG_PHASE_TIMING
+  __syncthreads();
+  PMG_PH(6);
+  if (threadIdx.x == 0 && (blockIdx.x % 512) == 0)
+    printf("PHASE fdm<%d,%d,%d> blk %d start %lld gather %lld xf %lld yf %lld z %lld yb %lld xb %lld\n", M0, M1, M2,
+           blockIdx.x, tph[0], tph[1] - tph[0], tph[2] - tph[1], tph[3] - tph[2], tph[4] - tph[3],
+           tph[5] - tph[4], tph[6] - tph[5]);
+#endif
+#undef PMG_PH
 }
 
 template <int M0, int M1, int M2>

@@ -238,4 +238,39 @@ cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double
   return cudaGetLastError();
 }
 
+// p-transfers for n_f > 17 (P = 32 level of c4: 33^3 fine, 17^3 coarse elements) as three
+// batched global line GEMMs each (Alg. 1 l.292 / l.299), spread over the whole GPU
+// instead of one CTA per element.  X1, X2: scratch of Ne * nf * nf * nc doubles each.
+cudaError_t launch_restrict_global(const LevelDev &Lf, int nc, const double *I, const double *rf,
+                                   double *fc, double *X1, double *X2, cudaStream_t s) {
+  const int nf = Lf.n;
+  const Blk B0 = {{nf, nf, nf}, {1, nf, nf * nf}};
+  const Blk B1 = {{nc, nf, nf}, {1, nc, nc * nf}};
+  const Blk B2 = {{nc, nc, nf}, {1, nc, nc * nc}};
+  const Blk B3 = {{nc, nc, nc}, {1, nc, nc * nc}};
+  const LineSpec rs = {nc, nf, I, 1, nc, nullptr, 0, 0, 0, 0};     // A[c][i] = I[i][c]
+  const long long b0 = (long long)nf * nf * nf, b1 = (long long)nc * nf * nf, b2 = (long long)nc * nc * nf,
+                  b3 = (long long)nc * nc * nc;
+  cudaError_t e;
+  if ((e = lines_global<0>(rf, b0, B0, rs, 0, Lf.Ne, GEpiStore{X1, b1, B1}, s))) return e;
+  if ((e = lines_global<1>(X1, b1, B1, rs, 0, Lf.Ne, GEpiStore{X2, b2, B2}, s))) return e;
+  return lines_global<2>(X2, b2, B2, rs, 0, Lf.Ne, GEpiStore{fc, b3, B3}, s);
+}
+
+cudaError_t launch_prolong_global(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                                  double *uf, double *X1, double *X2, cudaStream_t s) {
+  const int nf = Lf.n;
+  const Blk B0 = {{nc, nc, nc}, {1, nc, nc * nc}};
+  const Blk B1 = {{nf, nc, nc}, {1, nf, nf * nc}};
+  const Blk B2 = {{nf, nf, nc}, {1, nf, nf * nf}};
+  const Blk B3 = {{nf, nf, nf}, {1, nf, nf * nf}};
+  const LineSpec ps = {nf, nc, I, nc, 1, nullptr, 0, 0, 0, 0};     // A[i][c] = I[i][c]
+  const long long b0 = (long long)nc * nc * nc, b1 = (long long)nf * nc * nc, b2 = (long long)nf * nf * nc,
+                  b3 = (long long)nf * nf * nf;
+  cudaError_t e;
+  if ((e = lines_global<0>(uc, b0, B0, ps, 0, Lf.Ne, GEpiStore{X1, b1, B1}, s))) return e;
+  if ((e = lines_global<1>(X1, b1, B1, ps, 0, Lf.Ne, GEpiStore{X2, b2, B2}, s))) return e;
+  return lines_global<2>(X2, b2, B2, ps, 0, Lf.Ne, GEpiAcc{uf, b3, B3, 0}, s);     // u_f +=
+}
+
 }  // namespace pmg

@@ -28,7 +28,8 @@ __global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restr
 #pragma unroll
     for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
   const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
-  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
+  // !TR: blockIdx.y splits the element's DOFs (large elements fill the GPU); TR: gridDim.y = 1
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < n3; t += gridDim.y * blockDim.x) {
     const int i = t % n, j = (t / n) % n, k = t / (n * n);
     const int idx[3] = {i, j, k};
     const int nod[3] = {no0, no1, no2};
@@ -347,7 +348,7 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
   if (T) k_fold2<NN, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);                             \
   else k_fold2<NN, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
   if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
-    if (L.n == 33) k_fold2<33, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+    if (L.n == 33) k_fold2<33, false><<<dim3(L.Ne, 36), 256, 0, s>>>(L, Z, u, z, nullptr);
     else if (L.n == 5) k_fold2<5, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
     else if (L.n == 3) k_fold2<3, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
     else k_fold2<0, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
@@ -360,7 +361,10 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
     case 5: PMG_FOLD(5) break;
     case 9: PMG_FOLD(9) break;
     case 17: PMG_FOLD(17) break;
-    case 33: PMG_FOLD(33) break;
+    case 33:
+      if (T) k_fold2<33, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);
+      else k_fold2<33, false><<<dim3(L.Ne, 36), 256, 0, s>>>(L, Z, u, z, nullptr);
+      break;
     default: PMG_FOLD(0) break;
   }
 #undef PMG_FOLD

@@ -42,6 +42,11 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
 cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
                                 double *out, double *Cb, double *V, cudaStream_t s);
 bool fdm_mma_ok(const LevelDev &L);
+// p-transfers as batched global line GEMMs (n_f > 17); X1, X2: Ne * nf * nf * nc doubles each
+cudaError_t launch_restrict_global(const LevelDev &Lf, int nc, const double *I, const double *rf,
+                                   double *fc, double *X1, double *X2, cudaStream_t s);
+cudaError_t launch_prolong_global(const LevelDev &Lf, int nc, const double *I, const double *uc,
+                                  double *uf, double *X1, double *X2, cudaStream_t s);
 // Colored Schwarz step: 8 launches (parity classes of the element coordinates); same-colour
 // windows are node-disjoint, so each subdomain adds W du_s straight into u (no Z, no fold);
 // deterministic (fixed colour order).  Needs even n_e and 2 n_o <= n in every direction.
