@@ -299,6 +299,10 @@ int coarse_impl(dg_ctx *c, const double *f0, double *u0, cudaStream_t s) {
   double *part = wsp<double>(c, c->o_part);
   double *scal = wsp<double>(c, c->o_scal);
   double *G1 = wsp<double>(c, c->o_G1), *G2 = wsp<double>(c, c->o_G2);
+  if (pmg::coarse_one_ok(C)) {
+    LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_one(d0, C, f0, u0, s));
+    return PMG_OK;
+  }
   if (c->G[2] <= 32) {
     LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_fused(d0, C, f0, G1, G2, u0, s));
     c->launches += 4;   // launch_coarse_fused issues 5 kernels

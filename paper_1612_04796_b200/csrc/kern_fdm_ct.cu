@@ -294,7 +294,15 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>:
   PMG_PH(2);
   eoc_lines<1, SH, true, true>(X, Ss[1], st); __syncthreads();
   PMG_PH(3);
+#ifdef PMG_ZSPLIT
+  {   // z forward with the eigen-divide epilogue, then z backward (two pipelined passes)
+    EpiDivide dv{X, B, {lamc[0], lamc[1], lamc[2]}};
+    eoc_lines<2, SH, true, false>(X, Ss[2], dv); __syncthreads();
+    eoc_lines<2, SH, false, false>(X, Ss[2], st); __syncthreads();
+  }
+#else
   eoc_z_fused<SH>(X, Ss[2], lamc); __syncthreads();
+#endif
   PMG_PH(4);
   eoc_lines<1, SH, false, true>(X, Ss[1], st); __syncthreads();
   PMG_PH(5);

@@ -28,8 +28,11 @@ __global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restr
 #pragma unroll
     for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
   const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
-  // !TR: blockIdx.y splits the element's DOFs (large elements fill the GPU); TR: gridDim.y = 1
-  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < n3; t += gridDim.y * blockDim.x) {
+  // n = 33: blockIdx.y splits the element's DOFs (64 large elements must fill the GPU)
+  constexpr bool SPLIT = NT == 33 && !TR;
+  const int t0 = SPLIT ? blockIdx.y * blockDim.x + threadIdx.x : threadIdx.x;
+  const int dt = SPLIT ? gridDim.y * blockDim.x : blockDim.x;
+  for (int t = t0; t < n3; t += dt) {
     const int i = t % n, j = (t / n) % n, k = t / (n * n);
     const int idx[3] = {i, j, k};
     const int nod[3] = {no0, no1, no2};
@@ -200,6 +203,63 @@ __global__ void k_coarse_z(CoarseDev C, double *__restrict__ G) {
       if (lane < Gz) out += S[lane * Gz + k] * wk;
     }
     if (lane < Gz) G[cidx + lane * cols] = out;
+  }
+}
+
+// Whole coarse solve u_0 = A_0^+ f_0 in ONE CTA for small coarse grids (G_x G_y G_z <= 1024,
+// every G_d <= 32: c1, c4; at 16^3 (c2) one SM is slower than five launches): same passes and summation order as k_coarse_xf / k_lex_contract
+// / k_coarse_z / k_coarse_xb, staged in shared memory, so the 5-launch chain (launch-latency
+// bound at these sizes) becomes one launch.  smem: A, B (N each) | S_x, S_y, S_z | lam.
+__global__ void __launch_bounds__(1024) k_coarse_one(CoarseDev C, int nx, int ny,
+                                                     const double *__restrict__ f0,
+                                                     double *__restrict__ u0) {
+  extern __shared__ double sm[];
+  const int Gx = C.G[0], Gy = C.G[1], Gz = C.G[2];
+  const int N = Gx * Gy * Gz;
+  double *A = sm, *B = sm + N;
+  double *S[3] = {B + N, B + N + Gx * Gx, B + N + Gx * Gx + Gy * Gy};
+  double *lam[3] = {S[2] + Gz * Gz, S[2] + Gz * Gz + Gx, S[2] + Gz * Gz + Gx + Gy};
+  const int Gd[3] = {Gx, Gy, Gz};
+  for (int d = 0; d < 3; ++d) {
+    for (int i = threadIdx.x; i < Gd[d] * Gd[d]; i += blockDim.x) S[d][i] = C.S[d][i];
+    for (int i = threadIdx.x; i < Gd[d]; i += blockDim.x) lam[d][i] = C.lam[d][i];
+  }
+  for (int g = threadIdx.x; g < N; g += blockDim.x) {
+    const int X = g % Gx, Y = (g / Gx) % Gy, Z = g / (Gx * Gy);
+    A[g] = __ldg(f0 + coarse_elem_index(nx, ny, X, Y, Z));
+  }
+  __syncthreads();
+  // contraction along axis d of `in` into `out` (lexicographic x fastest)
+  auto pass = [&](const double *in, double *out, int d, bool forward) {
+    const int st = d == 0 ? 1 : (d == 1 ? Gx : Gx * Gy);
+    const int G = Gd[d];
+    const double *Sd = S[d];
+    for (int g = threadIdx.x; g < N; g += blockDim.x) {
+      const int o = (g / st) % G;
+      const double *src = in + (g - o * st);
+      double acc = 0;
+      if (forward) for (int k = 0; k < G; ++k) acc += Sd[k * G + o] * src[k * st];
+      else for (int k = 0; k < G; ++k) acc += Sd[o * G + k] * src[k * st];
+      out[g] = acc;
+    }
+    __syncthreads();
+  };
+  pass(A, B, 0, true);
+  pass(B, A, 1, true);
+  pass(A, B, 2, true);
+  for (int g = threadIdx.x; g < N; g += blockDim.x) {
+    const int a = g % Gx, b = (g / Gx) % Gy, c = g / (Gx * Gy);
+    B[g] = (a == 0 && b == 0 && c == 0) ? 0.0 : B[g] / (lam[0][a] + lam[1][b] + lam[2][c]);
+  }
+  __syncthreads();
+  pass(B, A, 2, false);
+  pass(A, B, 1, false);
+  for (int g = threadIdx.x; g < N; g += blockDim.x) {
+    const int X = g % Gx, Y = (g / Gx) % Gy, Z = g / (Gx * Gy);
+    const double *row = B + (g - X);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += S[0][X * Gx + k] * row[k];
+    u0[coarse_elem_index(nx, ny, X, Y, Z)] = acc;
   }
 }
 
@@ -382,6 +442,24 @@ cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, cons
   k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, axis, forward ? 1 : 0, in, out);
   return cudaGetLastError();
 }
+bool coarse_one_ok(const CoarseDev &C) {
+  return (long long)C.G[0] * C.G[1] * C.G[2] <= 1024 && C.G[0] <= 32 && C.G[1] <= 32 && C.G[2] <= 32;
+}
+
+cudaError_t launch_coarse_one(const LevelDev &L0, const CoarseDev &C, const double *f0, double *u0,
+                              cudaStream_t s) {
+  const int N = C.G[0] * C.G[1] * C.G[2];
+  const size_t sb = sizeof(double) * (2 * (size_t)N + C.G[0] * C.G[0] + C.G[1] * C.G[1] +
+                                      C.G[2] * C.G[2] + C.G[0] + C.G[1] + C.G[2]);
+  static bool cfg = false;
+  if (!cfg) {
+    cfg = true;
+    cudaFuncSetAttribute(k_coarse_one, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
+  k_coarse_one<<<1, 1024, sb, s>>>(C, L0.nx, L0.ny, f0, u0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const double *f0,
                                 double *G1, double *G2, double *u0, cudaStream_t s) {
   const long long N = (long long)C.G[0] * C.G[1] * C.G[2];

@@ -76,6 +76,10 @@ cudaError_t launch_lex_contract(const CoarseDev &C, int axis, bool forward, cons
 // whole coarse solve in 5 launches (needs 2 n_e <= 32 along z; see kernels.cu)
 cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const double *f0,
                                 double *G1, double *G2, double *u0, cudaStream_t s);
+// whole coarse solve in one CTA (G_x G_y G_z <= 1024, G_d <= 32)
+bool coarse_one_ok(const CoarseDev &C);
+cudaError_t launch_coarse_one(const LevelDev &L0, const CoarseDev &C, const double *f0, double *u0,
+                              cudaStream_t s);
 cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s);
 cudaError_t launch_coarse_scatter(const LevelDev &L0, const CoarseDev &C, const double *G,
                                   const double *mean, double *u0, cudaStream_t s);
