@@ -83,6 +83,101 @@ __global__ void k_apply(LevelDev L, const double *__restrict__ u, const double *
   }
 }
 
+// Even/odd line GEMM of the apply for n = 17 (H = 8).  The element stiffness rows of Eq. 7 are
+// centro-symmetric (D_{16-i,16-k} = D_{ik}, a_{16-i} = b_i, ap_{16-i} = -bp_i on the symmetric
+// GL/GLL nodes), so with e_k = u_k + u_{16-k}, o_k = u_k - u_{16-k}:
+//   out_i + out_{16-i} = sum_{k<8} (D_ik + D_{i,16-k}) e_k + 2 D_i8 u_8 + (a_i + b_i)(c1 + c3) + (ap_i - bp_i)(c2 - c4)
+//   out_i - out_{16-i} = sum_{k<8} (D_ik - D_{i,16-k}) o_k + (a_i - b_i)(c1 - c3) + (ap_i + bp_i)(c2 + c4)
+// Both halves take the same B fragments lo +- hi (K slots 0-7: (u_k, u_{16-k}); 8: (u_8, u_8);
+// 9: (c1, c3); 10: (c2, -c4), the transform stores -c4; 11: zero A column), so a tile needs 3 + 3
+// DMMAs (rows 0-7) plus an FMA tail for the middle row instead of 2 x 6.  The 1/2 of
+// out = (E +- O)/2 is folded into A.
+template <int DIR, bool FIRST>
+__device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
+                                           const double *__restrict__ Daug) {
+  constexpr int n = 17, n2 = n * n, H = 8, KA = n + 4;
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  constexpr int SO = DIR == 0 ? 1 : (DIR == 1 ? n : n2);
+  constexpr int SP = PD == 0 ? 1 : (PD == 1 ? n : n2);
+  constexpr int SQ = QD == 0 ? 1 : (QD == 1 ? n : n2);
+  constexpr int NCOL = n2, NT = (NCOL + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  // A fragments (row i = g for E and O; tail row 8 for E), K slot k = 4 ks + t
+  double aE[3], aO[3], at[3];
+#pragma unroll
+  for (int ks = 0; ks < 3; ++ks) {
+    const int k = ks * 4 + t;
+    auto coefE = [&](int i) {
+      const double *r = Daug + i * KA;
+      if (k < H) return 0.5 * (r[k] + r[n - 1 - k]);
+      if (k == H) return 0.5 * r[H];
+      if (k == 9) return 0.5 * (r[n] + r[n + 2]);
+      if (k == 10) return 0.5 * (r[n + 1] - r[n + 3]);
+      return 0.0;
+    };
+    const double *r = Daug + g * KA;
+    aE[ks] = coefE(g);
+    at[ks] = coefE(H);
+    if (k < H) aO[ks] = 0.5 * (r[k] - r[n - 1 - k]);
+    else if (k == 9) aO[ks] = 0.5 * (r[n] - r[n + 2]);
+    else if (k == 10) aO[ks] = 0.5 * (r[n + 1] + r[n + 3]);
+    else aO[ks] = 0.0;
+  }
+  // B sources: lo / hi offsets, from U (k <= 8, 11) or from the face coefficients Cf (k = 9, 10)
+  bool fromC[3];
+  int o1[3], o2[3];
+#pragma unroll
+  for (int ks = 0; ks < 3; ++ks) {
+    const int k = ks * 4 + t;
+    fromC[ks] = (k == 9 || k == 10);
+    if (k == 9) { o1[ks] = 0; o2[ks] = 2 * n2; }
+    else if (k == 10) { o1[ks] = n2; o2[ks] = 3 * n2; }
+    else { const int kk = k < H ? k : H; o1[ks] = kk * SO; o2[ks] = (n - 1 - kk) * SO; }
+  }
+  for (int tile = warp; tile < NT; tile += nw) {
+    const int nb = min(tile * 8 + g, NCOL - 1);
+    const int qb = nb / n, pb = nb - qb * n;
+    const double *xb = U + pb * SP + qb * SQ;
+    const double *cb = Cfd + pb + n * qb;
+    double bE[3], bO[3];
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) {
+      const double *src = fromC[ks] ? cb : xb;
+      const double v1 = src[o1[ks]], v2 = src[o2[ks]];
+      bE[ks] = v1 + v2;
+      bO[ks] = v1 - v2;
+    }
+    double cE[2] = {0.0, 0.0}, cO[2] = {0.0, 0.0};
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) {
+      dmma884(cE[0], cE[1], aE[ks], bE[ks]);
+      dmma884(cO[0], cO[1], aO[ks], bO[ks]);
+    }
+    double tl = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) tl = fma(at[ks], bE[ks], tl);
+    tl += __shfl_xor_sync(0xffffffffu, tl, 1);
+    tl += __shfl_xor_sync(0xffffffffu, tl, 2);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int nn = tile * 8 + 2 * t + j;
+      if (nn >= NCOL) continue;
+      const int q = nn / n, p = nn - q * n;
+      double *vb = V + p * SP + q * SQ;
+      const double lo = cE[j] + cO[j], hi = cE[j] - cO[j];
+      if (FIRST) { vb[g * SO] = lo; vb[(n - 1 - g) * SO] = hi; }
+      else { vb[g * SO] += lo; vb[(n - 1 - g) * SO] += hi; }
+    }
+    if (t == 0 && tile * 8 + g < NCOL) {
+      double *vb = V + pb * SP + qb * SQ + H * SO;
+      if (FIRST) *vb = tl;
+      else *vb += tl;
+    }
+  }
+}
+
 // smem: U (n^3) | V (n^3) | face coefficients 3 x 4 x n^2 | mass 3 x n
 // Per direction d the line GEMM is  V += M_p M_q [D | a ap b bp] [U-lines ; c1 c2 c3 c4]  where
 // c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
@@ -166,18 +261,31 @@ __global__ void __launch_bounds__(NT <= 9 ? 128 : 256, NT <= 9 ? 8 : 2) k_apply_
       C[0] = -0.5 * tdR - mu * tvR;
       C[n2] = 0.5 * tvR;
       C[2 * n2] = 0.5 * tdL - mu * tvL;
+#ifndef PMG_NO_APPLY_EO
+      C[3 * n2] = NT == 17 ? 0.5 * tvL : -0.5 * tvL;     // even/odd passes take -c4
+#else
       C[3 * n2] = -0.5 * tvL;
+#endif
     }
     __syncthreads();
     const Blk B = {{n, n, n}, {1, n, n2}};
-    EpiAcc acc{V, B, true};
-    LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
-    mma_lines_ct<0, n, n + 4>(U, B, lx, acc); __syncthreads();
-    acc.first = false;
-    LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
-    mma_lines_ct<1, n, n + 4>(U, B, ly, acc); __syncthreads();
-    LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
-    mma_lines_ct<2, n, n + 4>(U, B, lz, acc); __syncthreads();
+#ifndef PMG_NO_APPLY_EO
+    if constexpr (NT == 17) {            // even/odd passes (the transform stored -c4)
+      apply_eo17<0, true>(U, Cf, V, L.Daug[0]); __syncthreads();
+      apply_eo17<1, false>(U, Cf + 4 * n2, V, L.Daug[1]); __syncthreads();
+      apply_eo17<2, false>(U, Cf + 8 * n2, V, L.Daug[2]); __syncthreads();
+    } else
+#endif
+    {
+      EpiAcc acc{V, B, true};
+      LineSpec lx = {n, n, L.Daug[0], n + 4, 1, Cf, 4, n2, 1, n};
+      mma_lines_ct<0, n, n + 4>(U, B, lx, acc); __syncthreads();
+      acc.first = false;
+      LineSpec ly = {n, n, L.Daug[1], n + 4, 1, Cf + 4 * n2, 4, n2, 1, n};
+      mma_lines_ct<1, n, n + 4>(U, B, ly, acc); __syncthreads();
+      LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
+      mma_lines_ct<2, n, n + 4>(U, B, lz, acc); __syncthreads();
+    }
     // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism
     const long long g0 = (long long)e * n3;
     constexpr int UNR = 4;
