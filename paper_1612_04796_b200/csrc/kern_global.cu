@@ -122,6 +122,101 @@ __global__ void __launch_bounds__(256, 2) k_lines_global(const double *__restric
   }
 }
 
+// Even/odd variant for the fast-diagonalisation passes of odd windows (m = 2H+1, exact-parity
+// eigenvectors with even modes first; see k_fdm_eo in kern_fdm.cu): per (block, 8-column tile)
+// work item 2 x MT x KS DMMAs (m = 45: 36) instead of ceil(m/8) x ceil(m/4) (m = 45: 72).
+// Forward: b_E = x_k + x_{m-1-k}, b_O = x_k - x_{m-1-k}, k clamped to H, middle column of S_E^T
+// halved; backward: b_E = t_E[min(k,H)], b_O = t_O[min(k,H-1)]; x_a = P_a + Q_a, x_{m-1-a} = P_a - Q_a.
+template <int DIR, int MT, int KS, bool FWD, class Epi>
+__global__ void __launch_bounds__(256, 2) k_lines_global_eo(const double *__restrict__ X, long long xbs,
+                                                         Blk B, const double *__restrict__ S,
+                                                         int nblocks, Epi epi) {
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  const int m = B.m[DIR], H = m >> 1;
+  const int mp = B.m[PD], mq = B.m[QD];
+  const int ncol = mp * mq;
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)mp + 1u;
+  const int so = B.s[DIR], sp = B.s[PD], sq = B.s[QD];
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int ntiles = (ncol + 7) >> 3;
+  const long long nitems = (long long)nblocks * ntiles;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double aE[MT][KS], aO[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int o = mt * 8 + g, k = ks * 4 + t;
+      if (FWD) {
+        aE[mt][ks] = (o <= H && k <= H) ? __ldg(S + k * m + o) * (k == H ? 0.5 : 1.0) : 0.0;
+        aO[mt][ks] = (o < H && k < H) ? __ldg(S + k * m + H + 1 + o) : 0.0;
+      } else {
+        aE[mt][ks] = (o <= H && k <= H) ? __ldg(S + o * m + k) : 0.0;
+        aO[mt][ks] = (o < H && k < H) ? __ldg(S + o * m + H + 1 + k) : 0.0;
+      }
+    }
+  int off1[KS], off2[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = ks * 4 + t, kl = min(k, H);
+    if (FWD) { off1[ks] = kl * so; off2[ks] = (m - 1 - kl) * so; }
+    else { off1[ks] = kl * so; off2[ks] = (H + 1 + min(k, H - 1)) * so; }
+  }
+  for (long long it = wid; it < nitems; it += nwarps) {
+    const int tile = (int)(it % ntiles);
+    const long long blk = it / ntiles;
+    const int nb = min(tile * 8 + g, ncol - 1);
+    const int qb = __umulhi((unsigned)nb, magic), pb = nb - qb * mp;
+    const double *xb = X + blk * xbs + pb * sp + qb * sq;
+    double bE[KS], bO[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double v1 = __ldg(xb + off1[ks]), v2 = __ldg(xb + off2[ks]);
+      if (FWD) { bE[ks] = v1 + v2; bO[ks] = v1 - v2; }
+      else { bE[ks] = v1; bO[ks] = v2; }
+    }
+    double cE[MT][2], cO[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) { cE[mt][0] = cE[mt][1] = cO[mt][0] = cO[mt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        dmma884(cE[mt][0], cE[mt][1], aE[mt][ks], bE[ks]);
+        dmma884(cO[mt][0], cO[mt][1], aO[mt][ks], bO[ks]);
+      }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tile * 8 + 2 * t + j;
+      if (n >= ncol) continue;
+      const int q = __umulhi((unsigned)n, magic), p = n - q * mp;
+      const double cf = epi.template col<DIR>(blk, p, q);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        if (FWD) {
+          if (o <= H) epi.template put<DIR>(blk, o, p, q, cf, cE[mt][j]);
+          if (o < H) epi.template put<DIR>(blk, H + 1 + o, p, q, cf, cO[mt][j]);
+        } else if (o < H) {
+          epi.template put<DIR>(blk, o, p, q, cf, cE[mt][j] + cO[mt][j]);
+          epi.template put<DIR>(blk, m - 1 - o, p, q, cf, cE[mt][j] - cO[mt][j]);
+        } else if (o == H) {
+          epi.template put<DIR>(blk, o, p, q, cf, cE[mt][j]);
+        }
+      }
+    }
+  }
+}
+
+template <int DIR, bool FWD, class Epi>
+cudaError_t lines_global_eo(const double *X, long long xbs, const Blk &B, const double *S,
+                            int nblocks, const Epi &epi, cudaStream_t s) {
+  k_lines_global_eo<DIR, 3, 6, FWD, Epi><<<148 * 2, 256, 0, s>>>(X, xbs, B, S, nblocks, epi);
+  return cudaGetLastError();
+}
+
 template <int DIR, class Epi>
 cudaError_t lines_global(const double *X, long long xbs, const Blk &B, const LineSpec &ls,
                          long long ebs, int nblocks, const Epi &epi, cudaStream_t s) {
@@ -208,6 +303,20 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
   const long long total = (long long)L.Ne * L.Mw;
   k_gather_win<<<grid_for(total, 256), 256, 0, s>>>(L, r, X);
   const int *m = L.m;
+  bool eo = true;                         // odd windows with H <= 23 (MT 3, KS 6 tiles)
+  for (int d = 0; d < 3; ++d) eo = eo && (m[d] & 1) && m[d] / 2 >= 16 && m[d] / 2 <= 23;
+#ifdef PMG_NO_EO
+  eo = false;
+#endif
+  if (eo) {
+    cudaError_t e;
+    if ((e = lines_global_eo<0, true>(X, bs, B, L.S[0], L.Ne, GEpiStore{Y, bs, B}, s))) return e;
+    if ((e = lines_global_eo<1, true>(Y, bs, B, L.S[1], L.Ne, GEpiStore{X, bs, B}, s))) return e;
+    if ((e = lines_global_eo<2, true>(X, bs, B, L.S[2], L.Ne, GEpiDivide{Y, bs, B, {L.lam[0], L.lam[1], L.lam[2]}}, s))) return e;
+    if ((e = lines_global_eo<2, false>(Y, bs, B, L.S[2], L.Ne, GEpiStore{X, bs, B}, s))) return e;
+    if ((e = lines_global_eo<1, false>(X, bs, B, L.S[1], L.Ne, GEpiStore{Y, bs, B}, s))) return e;
+    return lines_global_eo<0, false>(Y, bs, B, L.S[0], L.Ne, GEpiWeight{Z, bs, B, {L.W[0], L.W[1], L.W[2]}}, s);
+  }
   auto fw = [&](int d) { return LineSpec{m[d], m[d], L.S[d], 1, m[d], nullptr, 0, 0, 0, 0}; };
   auto bw = [&](int d) { return LineSpec{m[d], m[d], L.S[d], m[d], 1, nullptr, 0, 0, 0, 0}; };
   cudaError_t e;
