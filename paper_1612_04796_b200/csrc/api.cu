@@ -28,10 +28,11 @@ struct LevelHost {
   int m[3] = {0, 0, 0};
   int Mw = 0;
   std::vector<double> mass[3], D[3], tr[3], S[3], lam[3], W[3], interp, nodes, Daug[3];
+  std::vector<double> Rz;    // 1/(lam_x[p] + lam_y[q] + lam_z[o]) at [(p + m_x q) m_z + o] (eigen-divide table)
   // workspace byte offsets
   size_t o_mass[3], o_D[3], o_tr[3], o_S[3], o_lam[3], o_W[3], o_Daug[3], o_interp = 0, o_nodes = 0;
   size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0, o_scr2 = 0, o_cb = 0, o_v = 0;
-  size_t o_x1 = 0, o_x2 = 0;   // transfer scratch (n > 17): Ne * n * n * n_c each
+  size_t o_x1 = 0, o_x2 = 0, o_Rz = 0;   // transfer scratch (n > 17): Ne * n * n * n_c each
   int fdm_path = 0;          // 0: DMMA in shared memory, 1: global-memory line GEMMs, 2: generic
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
@@ -111,6 +112,7 @@ pmg::LevelDev level_dev(const dg_ctx *c, int l) {
     d.W[k] = h.W[k].empty() ? nullptr : wsp<double>(c, h.o_W[k]);
     d.Daug[k] = wsp<double>(c, h.o_Daug[k]);
   }
+  d.Rz = h.Rz.empty() ? nullptr : wsp<double>(c, h.o_Rz);
   d.nodes = wsp<double>(c, h.o_nodes);
   d.Mw = h.Mw;
   return d;
@@ -160,6 +162,7 @@ void plan_workspace(dg_ctx *c) {
     h.o_T = p.dbl(Ne * 12 * n * n);
     if (l >= 1 && c->schwarz_ready) {
       h.o_Z = p.dbl(Ne * h.Mw);
+      h.o_Rz = p.dbl(h.Rz.size());
       size_t mma_words = (size_t)h.Mw;
       int mmax = 0;
       for (int d = 0; d < 3; ++d) {
@@ -529,6 +532,14 @@ int dg_schwarz_setup(dg_ctx *c, int mode, double value, int floor_layers) {
     }
     // A_ss regular: every eigenvalue sum lam_x + lam_y + lam_z > 0.  A single
     // direction may be singular (window = whole periodic line) if another one is not.
+    // eigen-divide table (exact reciprocal of the FP64 eigenvalue sums, rounded once)
+    h.Rz.assign((size_t)h.Mw, 0.0);
+    for (int q = 0; q < h.m[1]; ++q)
+      for (int pp = 0; pp < h.m[0]; ++pp)
+        for (int o = 0; o < h.m[2]; ++o) {
+          const ld sum = (ld)h.lam[0][pp] + (ld)h.lam[1][q] + (ld)h.lam[2][o];
+          h.Rz[((size_t)pp + (size_t)h.m[0] * q) * h.m[2] + o] = sum != 0 ? (double)(1 / sum) : 0.0;
+        }
     const ld smin = h.lam_min[0] + h.lam_min[1] + h.lam_min[2];
     const ld smax = h.lam_max[0] + h.lam_max[1] + h.lam_max[2];
     if (!(smin > 1e-13L * smax)) return fail(c, PMG_ESINGULAR, "restricted operator A_ss not regular");
@@ -602,6 +613,7 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
       if (e == cudaSuccess) e = up(h.o_Daug[d], h.Daug[d]);
     }
     if (e == cudaSuccess) e = up(h.o_interp, h.interp);
+    if (e == cudaSuccess && !h.Rz.empty()) e = up(h.o_Rz, h.Rz);
     if (e == cudaSuccess) e = up(h.o_nodes, h.nodes);
   }
   for (int d = 0; d < 3 && e == cudaSuccess; ++d) {

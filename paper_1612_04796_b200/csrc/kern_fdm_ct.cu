@@ -134,7 +134,8 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
 
 // z passes fused: forward S_z^T, eigen-divide, backward S_z on warp-private z columns
 template <class SH>
-__device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const double *const *lam) {
+__device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const double *const *lam,
+                                            const double *__restrict__ Rz) {
   constexpr int m = SH::template m<2>(), H = m / 2;
   constexpr int MT = (H + 1 + 7) / 8, KS = (H + 1 + 3) / 4;
   constexpr int MP = SH::template m<0>(), MQ = SH::template m<1>();
@@ -161,18 +162,24 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
     lo[ks] = kl * SO; hi[ks] = (m - 1 - kl) * SO;
     oo[ks] = (H + 1 + min(k, H - 1)) * SO;
   }
-  double lz[MT], lzo[MT];
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt) {
-    const int o = mt * 8 + g;
-    lz[mt] = lam[2][min(o, H)];
-    lzo[mt] = lam[2][H + 1 + min(o, H - 1)];
-  }
   for (int tile = warp; tile < NT; tile += NW) {
     const int nb = min(tile * 8 + g, NCOL - 1);
     const int qb = nb / MP, pb = nb - qb * MP;
     double *xb = X + pb + qb * SQ;
     double bE[KS], bO[KS], cE[MT][2], cO[MT][2];
+    // eigen-divide factors of this lane's outputs, fetched before the DMMAs (L1/L2 table)
+    double rE[MT][2], rO[MT][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = min(tile * 8 + 2 * t + j, NCOL - 1);
+      const double *rc = Rz + (long long)n * m;        // column n = p + MP q, p = x fastest
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int o = mt * 8 + g;
+        rE[mt][j] = __ldg(rc + min(o, H));
+        rO[mt][j] = __ldg(rc + H + 1 + min(o, H - 1));
+      }
+    }
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const double v1 = xb[lo[ks]], v2 = xb[hi[ks]];
@@ -196,12 +203,11 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
       if (n >= NCOL) continue;
       const int q = n / MP, p = n - q * MP;
       wb[j] = p + q * SQ;
-      const double cf = lam[0][p] + lam[1][q];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int o = mt * 8 + g;
-        if (o <= H) X[wb[j] + o * SO] = cE[mt][j] * rcp_nr(cf + lz[mt]);
-        if (o < H) X[wb[j] + (H + 1 + o) * SO] = cO[mt][j] * rcp_nr(cf + lzo[mt]);
+        if (o <= H) X[wb[j] + o * SO] = cE[mt][j] * rE[mt][j];
+        if (o < H) X[wb[j] + (H + 1 + o) * SO] = cO[mt][j] * rO[mt][j];
       }
     }
     __syncwarp();
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>:
     eoc_lines<2, SH, false, false>(X, Ss[2], st); __syncthreads();
   }
 #else
-  eoc_z_fused<SH>(X, Ss[2], lamc); __syncthreads();
+  eoc_z_fused<SH>(X, Ss[2], lamc, L.Rz); __syncthreads();
 #endif
   PMG_PH(4);
   eoc_lines<1, SH, false, true>(X, Ss[1], st); __syncthreads();

@@ -19,6 +19,7 @@ struct LevelDev {
   const double *nodes;     // n reference nodes
   const double *Daug[3];   // [D | a ap b bp], n x (n+4) row-major (apply line GEMM)
   int Mw;                  // m0*m1*m2
+  const double *Rz;        // eigen-divide table 1/(lam_x[p]+lam_y[q]+lam_z[o]) at [(p + m0 q) m2 + o]
 };
 
 struct CoarseDev {
