@@ -183,8 +183,9 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
 // c1..c4 are the neighbour-trace coefficients of the rank-2 couplings on the face point (p,q):
 // c1 = -tdR/2 - mu tvR, c2 = tvR/2, c3 = tdL/2 - mu tvL, c4 = -tvL/2.
 // NT = n (compile time, n = 2^l + 1 or 2), NC = (n + 1) / 2 the next-coarser n (fused restriction)
-template <int NT>
-__global__ void __launch_bounds__(NT <= 9 ? 128 : 256, NT <= 9 ? 8 : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+// WIDE: 256-thread CTAs for n <= 9 when the whole mesh is one wave (latency-bound small meshes)
+template <int NT, bool WIDE = false>
+__global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WIDE ? 4 : 8) : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
                                                       const double *__restrict__ T,
                                                       const double *__restrict__ f,
                                                       double *__restrict__ out,
@@ -415,11 +416,12 @@ static size_t apply_mma_smem(int n) {
   return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2);
 }
 
-template <int NT>
+template <int NT, bool WIDE>
 static int apply_grid(size_t sb, long long Ne) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_mma<NT>, NT <= 9 ? 128 : 256, sb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_mma<NT, WIDE>,
+                                                  (NT <= 9 && !WIDE) ? 128 : 256, sb);
     occ = std::max(occ, 1);
   }
   return (int)std::min<long long>(Ne, (long long)occ * num_sms());
@@ -428,10 +430,20 @@ static int apply_grid(size_t sb, long long Ne) {
 template <int NT>
 static void launch_apply_nt(const LevelDev &L, const double *u, const double *T, const double *f,
                             double *out, const double *I, double *fc, cudaStream_t s) {
-  // persistent grid: as many CTAs as fit on the device at once (occupancy x SMs), capped at Ne
+  // persistent grid: as many CTAs as fit on the device at once (occupancy x SMs), capped at Ne;
+  // a mesh that fits in one wave of 4 CTAs per SM gets 256-thread CTAs (latency-bound regime)
   const size_t sb = apply_mma_smem(NT);
+  if (NT <= 9 && L.Ne <= 4LL * num_sms()) {
+    static bool cfg = false;
+    if (!cfg) {
+      cfg = true;
+      cudaFuncSetAttribute(k_apply_mma<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
+    k_apply_mma<NT, true><<<apply_grid<NT, true>(sb, L.Ne), 256, sb, s>>>(L, u, T, f, out, I, fc);
+    return;
+  }
   const int threads = NT <= 9 ? 128 : 256;
-  k_apply_mma<NT><<<apply_grid<NT>(sb, L.Ne), threads, sb, s>>>(L, u, T, f, out, I, fc);
+  k_apply_mma<NT, false><<<apply_grid<NT, false>(sb, L.Ne), threads, sb, s>>>(L, u, T, f, out, I, fc);
 }
 
 bool apply_nt_ok(int n) { return n == 2 || n == 3 || n == 5 || n == 9 || n == 17; }

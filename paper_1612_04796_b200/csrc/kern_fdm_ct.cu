@@ -20,12 +20,14 @@ __host__ __device__ constexpr int plane_stride(int m0, int m1) {
   return m0 * m1 + ((4 - ((m0 * m1) & 15)) & 15);   // 4 mod 16 doubles: bank spread
 }
 
-template <int M0, int M1, int M2>
+// WIDE: 256 threads for small windows too — used when the whole grid fits in one wave (small
+// meshes, e.g. c2's 512 subdomains), where a CTA's latency, not the SM's throughput, sets the time.
+template <int M0, int M1, int M2, bool WIDE = false>
 struct Shape {
   static constexpr int S2 = plane_stride(M0, M1);
   static constexpr int Hmax = (M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2)) / 2;
-  static constexpr int THREADS = Hmax >= 8 ? 256 : 128;
-  static constexpr int MINB = Hmax >= 8 ? 2 : 8;
+  static constexpr int THREADS = (Hmax >= 8 || WIDE) ? 256 : 128;
+  static constexpr int MINB = Hmax >= 8 ? 2 : (WIDE ? 4 : 8);
   template <int D> __host__ __device__ static constexpr int m() { return D == 0 ? M0 : (D == 1 ? M1 : M2); }
   template <int D> __host__ __device__ static constexpr int s() { return D == 0 ? 1 : (D == 1 ? M0 : S2); }
 };
@@ -244,11 +246,11 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
 }
 
 // Shared memory: window X (S2 * M2, padded planes) | S_x, S_y, S_z | lam | W | gather offsets
-template <int M0, int M1, int M2>
-__global__ void __launch_bounds__(Shape<M0, M1, M2>::THREADS, Shape<M0, M1, M2>::MINB)
+template <int M0, int M1, int M2, bool WIDE>
+__global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1, M2, WIDE>::MINB)
     k_fdm_eoc(LevelDev L, const double *__restrict__ r, double *__restrict__ Z, int color,
               double *__restrict__ u) {
-  using SH = Shape<M0, M1, M2>;
+  using SH = Shape<M0, M1, M2, WIDE>;
   constexpr int S2 = SH::S2, Mw = M0 * M1 * M2;
   extern __shared__ double sm[];
   double *X = sm;
@@ -337,16 +339,26 @@ size_t eoc_smem() {
                            3 * (M0 + M1 + M2));
 }
 
-template <int M0, int M1, int M2>
-void eoc_launch(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
-                cudaStream_t s) {
+template <int M0, int M1, int M2, bool WIDE>
+void eoc_launch_t(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
+                  cudaStream_t s) {
   const size_t sb = eoc_smem<M0, M1, M2>();
   static bool cfg = false;
   if (!cfg) {
     cfg = true;
-    cudaFuncSetAttribute(k_fdm_eoc<M0, M1, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_fdm_eoc<M0, M1, M2, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
-  k_fdm_eoc<M0, M1, M2><<<grid, Shape<M0, M1, M2>::THREADS, sb, s>>>(L, r, Z, color, u);
+  k_fdm_eoc<M0, M1, M2, WIDE><<<grid, Shape<M0, M1, M2, WIDE>::THREADS, sb, s>>>(L, r, Z, color, u);
+}
+
+template <int M0, int M1, int M2>
+void eoc_launch(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
+                cudaStream_t s) {
+  // one wave of 128-thread CTAs would leave the SMs mostly idle: widen the CTAs instead
+  if (Shape<M0, M1, M2>::THREADS == 128 && grid <= 4 * num_sms())
+    eoc_launch_t<M0, M1, M2, true>(L, grid, r, Z, color, u, s);
+  else
+    eoc_launch_t<M0, M1, M2, false>(L, grid, r, Z, color, u, s);
 }
 
 }  // namespace
