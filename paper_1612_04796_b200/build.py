@@ -22,23 +22,26 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, extra=(), out=None):
+    """extra / out: diagnostic variants (-D switches) built into their own object dir and .so."""
+    lib = out or LIB
+    objdir = os.path.join(HERE, "build", os.path.basename(lib) + ".obj") if out else os.path.join(HERE, "build")
+    if not out and not force and not _stale():
         return LIB
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
 
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
     headers.append(os.path.join(ROOT, "include", "pmg_dg.h"))
 
     def compile_one(src):
-        obj = os.path.join(HERE, "build", src + ".o")
+        obj = os.path.join(objdir, src + ".o")
         if not force and os.path.exists(obj):
             t = os.path.getmtime(obj)
             if all(os.path.getmtime(d) <= t for d in headers + [os.path.join(CSRC, src)]):
                 return obj, subprocess.CompletedProcess([], 0, "", "")
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + FLAGS + list(extra) + ["-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, "-x", "cu"] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, "-x", "cu"] + FLAGS + list(extra) + ["-c", os.path.join(CSRC, src), "-o", obj]
         return obj, subprocess.run(cmd, capture_output=True, text=True)
 
     # translation units compile in parallel (the kernel files dominate the build time)
@@ -53,15 +56,19 @@ def build(force=False, verbose=False):
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs
                        + ["-lcudart"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH -DFOO=1 ...]   (variants: always a full rebuild)
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args or out is not None, verbose="-v" in args, extra=extra, out=out))

@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
 #endif
   fdm_offsets(L, e, offs);
   __syncthreads();
+#ifdef PMG_GATHER_ROWS
   {   // gather: one warp per window row (M0 <= 32), padded plane stride
     const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -292,6 +293,17 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
       if (lane < M0) cp_async8(X + lane + M0 * b + S2 * c, r + xa + yo[b] + zo[c]);
     }
   }
+#else
+  {   // gather: flat over the window (all 32 lanes of every cp.async busy: LDGSTS issue, not
+      // latency, bounds this phase — a row per warp left 32 - M0 lanes idle), padded plane stride
+    const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
+    for (int w = threadIdx.x; w < Mw; w += SH::THREADS) {
+      const int bc = w / M0, a = w - bc * M0;
+      const int c = bc / M1, b = bc - c * M1;
+      cp_async8(X + a + M0 * b + S2 * c, r + xo[a] + yo[b] + zo[c]);
+    }
+  }
+#endif
   cp_async_wait_all();
   __syncthreads();
   PMG_PH(1);
