@@ -218,6 +218,12 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
   __syncthreads();
   unsigned phase = 0;
+#ifdef PMG_PHASE_TIMING
+  long long tacc[7] = {0, 0, 0, 0, 0, 0, 0}, tp = clock64(), tq;
+#define PMG_APH(i) (tq = clock64(), tacc[i] += tq - tp, tp = tq)
+#else
+#define PMG_APH(i)
+#endif
   for (int e = blockIdx.x; e < L.Ne; e += gridDim.x, phase ^= 1u) {
     // TMA bulk staging: the element block and the six neighbour-trace segments (2 n^2 doubles,
     // 16-byte aligned) in 7 copies tracked by one mbarrier.  Element blocks (n^3 doubles, n odd)
@@ -254,6 +260,7 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
     __syncthreads();
     mbar_wait(mbar, phase);
     __syncthreads();
+    PMG_APH(0);
     for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
       const int d = t / n2, pp = t - d * n2;
       double *C = Cf + d * 4 * n2 + pp;
@@ -272,9 +279,12 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
     const Blk B = {{n, n, n}, {1, n, n2}};
 #ifndef PMG_NO_APPLY_EO
     if constexpr (NT == 17) {            // even/odd passes (the transform stored -c4)
+      PMG_APH(1);
       apply_eo17<0, true>(U, Cf, V, L.Daug[0]); __syncthreads();
+      PMG_APH(2);
       apply_eo17<1, false>(U, Cf + 4 * n2, V, L.Daug[1]); __syncthreads();
       apply_eo17<2, false>(U, Cf + 8 * n2, V, L.Daug[2]); __syncthreads();
+      PMG_APH(3);
     } else
 #endif
     {
@@ -287,9 +297,15 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
       LineSpec lz = {n, n, L.Daug[2], n + 4, 1, Cf + 8 * n2, 4, n2, 1, n};
       mma_lines_ct<2, n, n + 4>(U, B, lz, acc); __syncthreads();
     }
-    // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism
+    // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism:
+    // up to 10 f loads per thread in flight (the epilogue was a fifth of the kernel's time with 4)
     const long long g0 = (long long)e * n3;
-    constexpr int UNR = 4;
+#ifndef PMG_APPLY_UNR
+    constexpr int THR = (NT <= 9 && !WIDE) ? 128 : 256;
+    constexpr int UNR = NT == 17 ? 10 : (n3 + THR - 1) / THR;   // n = 17: 20 spills (measured 10 best)
+#else
+    constexpr int UNR = PMG_APPLY_UNR;
+#endif
     for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
       double fv[UNR];
 #pragma unroll
@@ -308,6 +324,8 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
         else out[g0 + t] = rr;
       }
     }
+    __syncthreads();
+    PMG_APH(4);
     if (NT > 2 && restrict_I) {
       // fused residual restriction f_c = (I^T (x) I^T (x) I^T) r (Alg. 1 l.292): r stays in V;
       // x pass (n -> nc) into U, y pass into Cf, z pass straight to the coarse vector
@@ -325,7 +343,14 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
       mma_lines_ct<2, NC, n>(Cf, T2, rx, s3);
     }
     __syncthreads();                   // U, V, Cf are reused by the next element
+    PMG_APH(5);
   }
+#ifdef PMG_PHASE_TIMING
+  if (threadIdx.x == 0 && (blockIdx.x % 64) == 0)
+    printf("APHASE apply<%d> blk %d restrict %d wait %lld coef %lld x %lld yz %lld epi %lld restr %lld\n", NT,
+           blockIdx.x, restrict_I != nullptr, tacc[0], tacc[1], tacc[2], tacc[3], tacc[4], tacc[5]);
+#endif
+#undef PMG_APH
 }
 
 // Face traces with the element staged in shared memory (coalesced loads).

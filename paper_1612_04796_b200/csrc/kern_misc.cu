@@ -10,8 +10,9 @@ namespace {
 // Register-only fold: one thread per DOF issues all (up to 27) predicated loads of the
 // weighted window values that cover it before summing them in a fixed order -> maximal
 // memory-level parallelism, deterministic result.  NT = compile-time n (fast index math).
+// Min 4 CTAs/SM (<= 64 registers): measured 0.515 vs 0.545 ms per cycle at c3's top level.
 template <int NT, bool TR>
-__global__ void __launch_bounds__(256) k_fold2(LevelDev L, const double *__restrict__ Z,
+__global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__restrict__ Z,
                                                double *__restrict__ u, int zero,
                                                double *__restrict__ T) {
   extern __shared__ double sm[];          // TR: the folded element (n^3) + trace table (12 n)
