@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "kcommon.cuh"
+#include "colmap17.cuh"
 
 namespace pmg {
 namespace {
@@ -92,9 +93,12 @@ __global__ void k_apply(LevelDev L, const double *__restrict__ u, const double *
 // 9: (c1, c3); 10: (c2, -c4), the transform stores -c4; 11: zero A column), so a tile needs 3 + 3
 // DMMAs (rows 0-7) plus an FMA tail for the middle row instead of 2 x 6.  The 1/2 of
 // out = (E +- O)/2 is folded into A.
+// cmap: tile slot -> column p + n q (scripts/gen_colmap17.py): tiles whose base addresses are
+// spread over the 16 double banks, so the B loads and the C stores are conflict free.
 template <int DIR, bool FIRST>
 __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
-                                           const double *__restrict__ Daug) {
+                                           const double *__restrict__ Daug,
+                                           const unsigned short *cmap) {
   constexpr int n = 17, n2 = n * n, H = 8, KA = n + 4;
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
   constexpr int SO = DIR == 0 ? 1 : (DIR == 1 ? n : n2);
@@ -136,7 +140,11 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     else { const int kk = k < H ? k : H; o1[ks] = kk * SO; o2[ks] = (n - 1 - kk) * SO; }
   }
   for (int tile = warp; tile < NT; tile += nw) {
+#ifndef PMG_APPLY_NOCMAP
+    const int nb = cmap[tile * 8 + g];
+#else
     const int nb = min(tile * 8 + g, NCOL - 1);
+#endif
     const int qb = nb / n, pb = nb - qb * n;
     const double *xb = U + pb * SP + qb * SQ;
     const double *cb = Cfd + pb + n * qb;
@@ -162,8 +170,13 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int nn = tile * 8 + 2 * t + j;
-      if (nn >= NCOL) continue;
+      const int slot = tile * 8 + 2 * t + j;
+      if (slot >= NCOL) continue;
+#ifndef PMG_APPLY_NOCMAP
+      const int nn = cmap[slot];
+#else
+      const int nn = slot;
+#endif
       const int q = nn / n, p = nn - q * n;
       double *vb = V + p * SP + q * SQ;
       const double lo = cE[j] + cO[j], hi = cE[j] - cO[j];
@@ -197,6 +210,7 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   // smem: U staging (n^3 + 2, 16-byte aligned superset of the element) | V | Cf | mass | mbarrier
   double *Us = sm, *V = sm + n3 + 2, *Cf = V + n3, *ms = Cf + 12 * n2;
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(ms + 3 * n);
+  unsigned short *cmap = reinterpret_cast<unsigned short *>(mbar + 1);      // n = 17 only
   const int edim[3] = {L.nx, L.ny, L.nz};
   const unsigned tbytes = 16u * n2;                                // 2 n^2 doubles per segment
   // Persistent: CTA b handles elements b, b + grid, ...  While element e is computed, the next
@@ -216,6 +230,8 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   };
   if (threadIdx.x == 0) mbar_init(mbar, 1);
   for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
+  if constexpr (NT == 17)
+    for (int i = threadIdx.x; i < PMG_COLMAP17_LEN; i += blockDim.x) cmap[i] = kColMap17[i];
   __syncthreads();
   unsigned phase = 0;
 #ifdef PMG_PHASE_TIMING
@@ -280,10 +296,10 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
 #ifndef PMG_NO_APPLY_EO
     if constexpr (NT == 17) {            // even/odd passes (the transform stored -c4)
       PMG_APH(1);
-      apply_eo17<0, true>(U, Cf, V, L.Daug[0]); __syncthreads();
+      apply_eo17<0, true>(U, Cf, V, L.Daug[0], cmap); __syncthreads();
       PMG_APH(2);
-      apply_eo17<1, false>(U, Cf + 4 * n2, V, L.Daug[1]); __syncthreads();
-      apply_eo17<2, false>(U, Cf + 8 * n2, V, L.Daug[2]); __syncthreads();
+      apply_eo17<1, false>(U, Cf + 4 * n2, V, L.Daug[1], cmap); __syncthreads();
+      apply_eo17<2, false>(U, Cf + 8 * n2, V, L.Daug[2], cmap); __syncthreads();
       PMG_APH(3);
     } else
 #endif
@@ -438,7 +454,7 @@ bool apply_pipe_ok(const LevelDev &L) { return L.n == 3 || L.n == 5 || L.n == 9 
 
 static size_t apply_mma_smem(int n) {
   const size_t n2 = (size_t)n * n, n3 = n2 * n;
-  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2);
+  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2) + 2 * PMG_COLMAP17_LEN;
 }
 
 template <int NT, bool WIDE>
