@@ -317,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
                       else "step = one V(1,1) cycle"),
                    "cycles_timed": cycles,
                    "overlap": {"mode": c.overlap.mode, "value": c.overlap.value, "floor": c.overlap.floor},
-                   "l2": "inputs larger than L2 (u, f, r: %.0f MB each); no flush" % (N * 8 / 1e6),
+                   "l2": l2_note(N, dev),
                    "parallelism": "replicas" if world > 1 else "single"},
         "e2e": {"value": N * world / (e2e_ms / 1e3), "unit": "DOF/s", "h2d_bytes_per_step": 16 * N,
                 "d2h_bytes_per_step": 8 * N},
@@ -412,6 +412,16 @@ def run_reference(args, rank, world):
             "config": {"workload": "%s (CPU oracle sample)" % args.config},
             "cpu_baseline": {"value": v, "unit": "DOF/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def l2_note(N, dev):
+    """How the timed iterations relate to L2 (no flush is done either way)."""
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    mb = N * 8 / 1e6
+    if N * 8 > l2:
+        return "inputs larger than L2 (u, f, r: %.0f MB each, L2 %.0f MB); no flush" % (mb, l2 / 1e6)
+    return ("vectors fit in L2 (u, f, r: %.1f MB each, L2 %.0f MB); no flush: L2-warm iterations "
+            "(a parity config; the headline c3 streams from HBM)" % (mb, l2 / 1e6))
 
 
 def main():

@@ -10,9 +10,13 @@ namespace {
 // Fused correction prolongation + face traces (Alg. 1 l.299 followed by the trace pass of the
 // post-smoothing residual): u_f += (I (x) I (x) I) u_c with three DMMA line GEMMs in shared
 // memory, u_f written back, and the traces of the new u_f emitted for the residual.
-// smem: Uc (nc^3) | T1 (nf nc^2) | T2 (nf^2 nc) | U (nf^3) | trs (12 nf)
+// smem: A = Uc (nc^3), later T2 (nf^2 nc) | U (nf^3) | T1 (nf nc^2) | trs (12 nf): T2 reuses the
+// dead Uc region, which brings n = 17 to 73 KB and 3 CTAs per SM
+#ifndef PMG_PT_MINB
+#define PMG_PT_MINB 3
+#endif
 template <int KSMAX>
-__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_PT_MINB) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
                                                         const double *__restrict__ uc,
                                                         double *__restrict__ uf,
                                                         double *__restrict__ T) {
@@ -20,8 +24,9 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : 2) k_
   const int nf = L.n, n2 = nf * nf, n3 = n2 * nf;
   const int c3 = nc * nc * nc;
   const int c3p = (c3 + 3) & ~1;                // staging capacities (16-byte aligned regions)
-  double *Ucs = sm, *Us = Ucs + c3p;
-  double *T1 = Us + ((n3 + 3) & ~1), *T2 = T1 + nf * nc * nc, *trs = T2 + nf * nf * nc;
+  const int ap = (max(c3p, nf * nf * nc) + 1) & ~1;
+  double *Ucs = sm, *T2 = sm, *Us = sm + ap;
+  double *T1 = Us + ((n3 + 3) & ~1), *trs = T1 + nf * nc * nc;
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * nf);
   const int e = blockIdx.x;
   const BulkPlan bc = bulk_plan(Ucs, uc + (long long)e * c3, c3, uc + (long long)L.Ne * c3);
@@ -120,8 +125,10 @@ static void configure_smem() {
 }
 
 static size_t prolong_traces_smem(int nf, int nc) {
-  return sizeof(double) * ((size_t)nc * nc * nc + 4 + (size_t)nf * nc * nc + (size_t)nf * nf * nc +
-                           (size_t)nf * nf * nf + 4 + 12 * (size_t)nf + 2);
+  const size_t c3p = ((size_t)nc * nc * nc + 3) & ~(size_t)1;
+  const size_t ap = (std::max(c3p, (size_t)nf * nf * nc) + 1) & ~(size_t)1;
+  return sizeof(double) * (ap + (((size_t)nf * nf * nf + 3) & ~(size_t)1) + (size_t)nf * nc * nc +
+                           12 * (size_t)nf + 2);
 }
 
 bool prolong_traces_ok(const LevelDev &Lf, int nc) {
