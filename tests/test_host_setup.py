@@ -79,3 +79,20 @@ def test_tables_match_oracle(name):
                 assert np.max(np.abs(S.T @ (M1[win][:, None] * S) - np.eye(m))) < 1e-13
                 assert np.allclose(g.table(l, d, 5), weights_1d(c.basis, P, res[d][0], res[d][1]),
                                    atol=1e-15, rtol=0)
+
+
+def test_colmap17_table_is_a_conflict_free_permutation():
+    """csrc/colmap17.cuh (the n = 17 apply's tile order) equals what scripts/gen_colmap17.py
+    builds: a permutation of the 289 line columns in 36 full tiles (+ one single-column tile)
+    whose B-load and C-store bank residues are distinct per half-warp (the generator's check)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gen_colmap17", os.path.join(ROOT, "scripts", "gen_colmap17.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    tab = gen.build()
+    gen.check(tab)
+    hdr = open(os.path.join(ROOT, "paper_1612_04796_b200", "csrc", "colmap17.cuh")).read()
+    body = re.search(r"kColMap17\[(\d+)\] = \{([^}]*)\}", hdr)
+    assert int(body.group(1)) == len(tab) == 296
+    assert [int(x) for x in body.group(2).split(",")] == tab
+    assert sorted(tab[:289]) == list(range(289)) and set(tab[289:]) == {tab[288]}
