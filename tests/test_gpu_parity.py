@@ -409,3 +409,25 @@ def test_workspace_and_state_errors():
     u = torch.zeros(g.ndofs(), dtype=torch.float64, device="cuda")
     with pytest.raises(PMGError):
         g.apply(u)                                   # workspace not bound -> PMG_ESTATE
+
+
+# ---- ragged (non-cubic) element grids with the benchmark window shapes: the compile-time
+# Schwarz kernels (23^3, 13^3, 11x27x27, ...), the n = 17 apply column table and the 3-CTA
+# prolongation on grids whose element counts per direction differ (periodic wrap per axis)
+RAGGED = [("c3", (3, 4, 3)), ("c5", (4, 3, 5)), ("c2", (5, 3, 4))]
+
+
+@pytest.mark.parametrize("name,ne", RAGGED, ids=[r[0] for r in RAGGED])
+def test_ragged_grids_benchmark_shapes(name, ne):
+    c = get_config(name, ne)
+    g = _gpu(c)
+    H = _oracle(c)
+    u = uniform_vector(c.ndofs, 1)
+    assert _rel(_n(g.apply(_t(u))), H.apply(H.L, u)) <= TOL
+    f = uniform_zero_mean(c.ndofs, 0)
+    ug = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    uo = np.zeros_like(f)
+    for _ in range(2):
+        g.pmg_vcycle(ug, _t(f))
+        uo = mg.vcycle(H, uo, f)
+    assert _rel(_n(ug), uo) <= _tol(c.name)
