@@ -42,6 +42,7 @@ _sig = {
     "dg_profile": (_i, [_vp, _i]),
     "dg_set_graphs": (_i, [_vp, _i]),
     "dg_set_colored": (_i, [_vp, _i]),
+    "dg_set_fused_fold": (_i, [_vp, _i]),
     "dg_profile_read": (_i, [_vp, _dp, C.POINTER(_ll), _i]),
     "pmg_fp64_peak": (_i, [_i, _dp, _vp]),
     "dg_last_error": (C.c_char_p, [_vp]),
@@ -62,6 +63,20 @@ class PMGError(RuntimeError):
 
 
 def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _vec(t, n, what="vector"):
+    """Pointer of a caller-owned device vector after the ABI's contract checks: CUDA, float64,
+    contiguous, exactly n entries (a wrong tensor would otherwise read/write out of bounds)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("%s: expected a torch.Tensor" % what)
+    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("%s: need a contiguous CUDA float64 tensor (got %s, %s, contiguous=%s)"
+                         % (what, t.device, t.dtype, t.is_contiguous()))
+    if t.numel() != n:
+        raise ValueError("%s: %d entries, the level has %d DOF" % (what, t.numel(), n))
     return C.c_void_p(t.data_ptr())
 
 
@@ -123,6 +138,9 @@ class DG:
     def set_colored(self, enable=True):
         self._check(lib.dg_set_colored(self._c, 1 if enable else 0))
 
+    def set_fused_fold(self, enable=True):
+        self._check(lib.dg_set_fused_fold(self._c, 1 if enable else 0))
+
     def set_graphs(self, enable=True):
         self._check(lib.dg_set_graphs(self._c, 1 if enable else 0))
 
@@ -150,48 +168,59 @@ class DG:
     def apply(self, u, level=None, out=None):
         level = self.L if level is None else level
         out = self.empty(level) if out is None else out
-        self._check(lib.dg_apply(self._c, level, _ptr(u), _ptr(out), _stream()))
+        n = self.ndofs(level)
+        self._check(lib.dg_apply(self._c, level, _vec(u, n, "u"), _vec(out, n, "out"), _stream()))
         return out
 
     def residual(self, u, f, level=None, out=None):
         level = self.L if level is None else level
         out = self.empty(level) if out is None else out
-        self._check(lib.dg_residual(self._c, level, _ptr(u), _ptr(f), _ptr(out), _stream()))
+        n = self.ndofs(level)
+        self._check(lib.dg_residual(self._c, level, _vec(u, n, "u"), _vec(f, n, "f"), _vec(out, n, "out"),
+                                    _stream()))
         return out
 
     def schwarz_smooth(self, u, f, steps=1, level=None):
         level = self.L if level is None else level
-        self._check(lib.schwarz_smooth(self._c, level, _ptr(u), _ptr(f), int(steps), _stream()))
+        n = self.ndofs(level)
+        self._check(lib.schwarz_smooth(self._c, level, _vec(u, n, "u"), _vec(f, n, "f"), int(steps), _stream()))
         return u
 
     def prolongate_add(self, uc, uf, level):
-        self._check(lib.dg_prolongate_add(self._c, level, _ptr(uc), _ptr(uf), _stream()))
+        self._check(lib.dg_prolongate_add(self._c, level, _vec(uc, self.ndofs(level - 1), "uc"),
+                                          _vec(uf, self.ndofs(level), "uf"), _stream()))
         return uf
 
     def restrict(self, rf, level, out=None):
         out = self.empty(level - 1) if out is None else out
-        self._check(lib.dg_restrict(self._c, level, _ptr(rf), _ptr(out), _stream()))
+        self._check(lib.dg_restrict(self._c, level, _vec(rf, self.ndofs(level), "rf"),
+                                    _vec(out, self.ndofs(level - 1), "out"), _stream()))
         return out
 
     def coarse_solve(self, f0, out=None):
         out = self.empty(0) if out is None else out
-        self._check(lib.dg_coarse_solve(self._c, _ptr(f0), _ptr(out), _stream()))
+        n = self.ndofs(0)
+        self._check(lib.dg_coarse_solve(self._c, _vec(f0, n, "f0"), _vec(out, n, "out"), _stream()))
         return out
 
     def set_schedule(self, nu1, nu2):
+        if len(nu1) != self.L + 1 or len(nu2) != self.L + 1:
+            raise ValueError("set_schedule: nu1, nu2 need L+1 = %d entries" % (self.L + 1))
         a = (C.c_int * len(nu1))(*nu1)
         b = (C.c_int * len(nu2))(*nu2)
         self._check(lib.dg_set_schedule(self._c, a, b))
 
     def pmg_vcycle(self, u, f):
-        self._check(lib.pmg_vcycle(self._c, _ptr(u), _ptr(f), _stream()))
+        n = self.ndofs()
+        self._check(lib.pmg_vcycle(self._c, _vec(u, n, "u"), _vec(f, n, "f"), _stream()))
         return u
 
     def pcg_solve(self, u, f, rtol=1e-10, maxit=100):
         import numpy as np
         it = C.c_int(0)
         hist = np.zeros(maxit + 1)
-        rc = lib.pcg_solve(self._c, _ptr(u), _ptr(f), float(rtol), int(maxit), C.byref(it),
+        n = self.ndofs()
+        rc = lib.pcg_solve(self._c, _vec(u, n, "u"), _vec(f, n, "f"), float(rtol), int(maxit), C.byref(it),
                            hist.ctypes.data_as(_dp), _stream())
         if rc and rc != 7:
             self._check(rc)
@@ -200,17 +229,18 @@ class DG:
     def dot(self, x, y, level=None):
         level = self.L if level is None else level
         v = C.c_double(0)
-        self._check(lib.dg_dot(self._c, level, _ptr(x), _ptr(y), C.byref(v), _stream()))
+        n = self.ndofs(level)
+        self._check(lib.dg_dot(self._c, level, _vec(x, n, "x"), _vec(y, n, "y"), C.byref(v), _stream()))
         return v.value
 
     def project_mean(self, v, level=None):
         level = self.L if level is None else level
-        self._check(lib.dg_project_mean(self._c, level, _ptr(v), _stream()))
+        self._check(lib.dg_project_mean(self._c, level, _vec(v, self.ndofs(level), "v"), _stream()))
         return v
 
     def rhs_sin(self, amp, kx, ky, kz, out=None):
         out = self.empty() if out is None else out
-        self._check(lib.dg_rhs_sin(self._c, float(amp), float(kx), float(ky), float(kz), _ptr(out),
+        self._check(lib.dg_rhs_sin(self._c, float(amp), float(kx), float(ky), float(kz), _vec(out, self.ndofs(), "out"),
                                    _stream()))
         return out
 

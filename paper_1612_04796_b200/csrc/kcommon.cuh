@@ -56,6 +56,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned pha
                  : "=r"(done) : "r"(smem_addr(mbar)), "r"(phase) : "memory");
 }
 
+// Order this thread's (and, after a CTA barrier, the CTA's) generic-proxy shared-memory accesses
+// before subsequent async-proxy (cp.async.bulk) writes to the same buffer (PTX cross-proxy rule).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // L2 prefetch of a 16-byte aligned block (cp.async.bulk.prefetch.L2; no shared memory used)
 __device__ __forceinline__ void prefetch_l2(const void *src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

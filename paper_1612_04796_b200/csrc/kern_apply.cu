@@ -249,6 +249,9 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
     const bool tail_ok = u_plan(e, pre, ucount);
     double *U = Us + pre;
     if (threadIdx.x == 0) {
+      // the previous element's generic stores to Us / Cf (coefficient rewrite, fused restriction,
+      // cp.async fallback) were ordered by the loop-end barrier; order them before the bulk writes
+      fence_proxy_async_smem();
       mbar_expect_tx(mbar, (tail_ok ? ucount * 8u : 0u) + 6u * tbytes);
       if (tail_ok) bulk_g2s(Us, ue - pre, ucount * 8u, mbar);
       for (int d = 0; d < 3; ++d) {
