@@ -33,7 +33,6 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fused-fold", action="store_true", help="A/B: separate Schwarz fold launch")
     ap.add_argument("--profile-kernels", action="store_true", default=True)
     return ap.parse_args()
 
@@ -155,8 +154,6 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
     c = get_config(args.config)
     g = DG(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
-    if args.no_fused_fold:
-        g.set_fused_fold(False)
     N = g.ndofs()
     from paper_1612_04796_b200.binding import fp64_peak_tflops
     peak_dfma = max(fp64_peak_tflops(False) for _ in range(3))

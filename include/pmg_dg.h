@@ -117,14 +117,6 @@ int dg_set_graphs(dg_ctx *ctx, int enable);
  * weighted windows are stored and a deterministic pull kernel folds them. */
 int dg_set_colored(dg_ctx *ctx, int enable);
 
-/* Fused Schwarz step (default ON; the weighted scatter-add of Eq. 10): on the
- * levels whose window shape has a compile-time kernel, one launch solves every subdomain AND
- * folds the weighted windows into u — the CTA that completes an element's 27 contributions sums
- * them in the same fixed order as the separate fold kernel (bit-identical results), and the
- * weighted windows are read back from L2 and discarded there instead of round-tripping through
- * HBM.  enable = 0: two launches (solve, then fold).  Host-only; drops cached graphs. */
-int dg_set_fused_fold(dg_ctx *ctx, int enable);
-
 /* pmg_vcycle — one multigrid V-cycle, Algorithm 1, in place on u
  * (top level), with the schedule above.  f is read-only. */
 int pmg_vcycle(dg_ctx *ctx, double *u, const double *f, void *stream);

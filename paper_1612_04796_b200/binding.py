@@ -42,7 +42,6 @@ _sig = {
     "dg_profile": (_i, [_vp, _i]),
     "dg_set_graphs": (_i, [_vp, _i]),
     "dg_set_colored": (_i, [_vp, _i]),
-    "dg_set_fused_fold": (_i, [_vp, _i]),
     "dg_profile_read": (_i, [_vp, _dp, C.POINTER(_ll), _i]),
     "pmg_fp64_peak": (_i, [_i, _dp, _vp]),
     "dg_last_error": (C.c_char_p, [_vp]),
@@ -137,9 +136,6 @@ class DG:
 
     def set_colored(self, enable=True):
         self._check(lib.dg_set_colored(self._c, 1 if enable else 0))
-
-    def set_fused_fold(self, enable=True):
-        self._check(lib.dg_set_fused_fold(self._c, 1 if enable else 0))
 
     def set_graphs(self, enable=True):
         self._check(lib.dg_set_graphs(self._c, 1 if enable else 0))

@@ -34,8 +34,6 @@ struct LevelHost {
   size_t o_u = 0, o_f = 0, o_r = 0, o_T = 0, o_Z = 0, o_scr = 0, o_scr2 = 0, o_cb = 0, o_v = 0;
   size_t o_x1 = 0, o_x2 = 0, o_Rz = 0;   // transfer scratch (n > 17): Ne * n * n * n_c each
   int fdm_path = 0;          // 0: DMMA in shared memory, 1: global-memory line GEMMs, 2: generic
-  bool fused = false;        // fused Schwarz step (solve + fold in one launch, pmg::launch_fdm_fold)
-  int Zs = 0;                // Z window stride (doubles)
   bool fdm_smem = false;
   size_t fdm_smem_bytes = 0;
   ld lam_min[3] = {0, 0, 0}, lam_max[3] = {0, 0, 0};
@@ -61,8 +59,6 @@ struct dg_ctx {
   size_t o_S0[3], o_lam0[3], o_G1 = 0, o_G2 = 0;
   // PCG + reductions
   size_t o_pr, o_pz, o_pp, o_pq, o_prold, o_part, o_scal;
-  size_t o_cnt = 0;          // 2 Ne fold counters of the fused Schwarz step (zero between launches)
-  bool fused_fold = true;    // dg_set_fused_fold
   size_t ws_bytes = 0;
   char *ws = nullptr;
   std::vector<int> nu1, nu2;
@@ -119,7 +115,6 @@ pmg::LevelDev level_dev(const dg_ctx *c, int l) {
   d.Rz = h.Rz.empty() ? nullptr : wsp<double>(c, h.o_Rz);
   d.nodes = wsp<double>(c, h.o_nodes);
   d.Mw = h.Mw;
-  d.Zs = h.Zs ? h.Zs : h.Mw;
   return d;
 }
 
@@ -166,9 +161,7 @@ void plan_workspace(dg_ctx *c) {
     h.o_r = p.dbl(h.N);
     h.o_T = p.dbl(Ne * 12 * n * n);
     if (l >= 1 && c->schwarz_ready) {
-      h.fused = pmg::fdm_fold_ok(n, h.m);
-      h.Zs = h.fused ? (h.Mw + 15) & ~15 : h.Mw;     // whole 128-byte lines per window (L2 discard)
-      h.o_Z = p.dbl(Ne * h.Zs);
+      h.o_Z = p.dbl(Ne * h.Mw);
       h.o_Rz = p.dbl(h.Rz.size());
       size_t mma_words = (size_t)h.Mw;
       int mmax = 0;
@@ -207,7 +200,6 @@ void plan_workspace(dg_ctx *c) {
   c->o_prold = p.dbl(NL);
   c->o_part = p.dbl(2 * 2048);
   c->o_scal = p.dbl(64);
-  c->o_cnt = p.take(sizeof(unsigned) * 2 * (size_t)Ne);
   c->ws_bytes = p.off + 256;
 }
 
@@ -289,12 +281,6 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
       LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_colored(d, rin, u, s));
       c->launches += 7;
       if (emit) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
-      continue;
-    }
-    if (h.fused && c->fused_fold) {
-      // one launch: subdomain solves + fold (+ traces of the new u) — Z stays in L2
-      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_fold(d, rin, Z, u, zero, emit ? T : nullptr,
-                                                   wsp<unsigned>(c, c->o_cnt), s));
       continue;
     }
     if (h.fdm_path == 1) {
@@ -634,7 +620,6 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
     e = up(c->o_S0[d], c->S0[d]);
     if (e == cudaSuccess) e = up(c->o_lam0[d], c->lam0[d]);
   }
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + c->o_cnt, 0, sizeof(unsigned) * 2 * (size_t)c->ne[0] * c->ne[1] * c->ne[2], s);
   if (e == cudaSuccess && !c->host_pinned) e = cudaMallocHost(&c->host_pinned, 64 * sizeof(double));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // host vectors must outlive the copies
   if (e != cudaSuccess) {
@@ -818,14 +803,6 @@ long long dg_launch_count(const dg_ctx *c) { return c ? c->launches : -1; }
 int dg_set_colored(dg_ctx *c, int enable) {
   if (!c) return PMG_EINVAL;
   c->colored = enable != 0;
-  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
-  c->graph_cache.clear();
-  return PMG_OK;
-}
-
-int dg_set_fused_fold(dg_ctx *c, int enable) {
-  if (!c) return PMG_EINVAL;
-  c->fused_fold = enable != 0;
   for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
   c->graph_cache.clear();
   return PMG_OK;

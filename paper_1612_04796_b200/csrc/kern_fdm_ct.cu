@@ -245,109 +245,11 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
   }
 }
 
-// ---- fused fold (the weighted scatter-add of Eq. 10) -----------------------
-// Fold of element e from the weighted windows of its 27 covering subdomains: the same fixed
-// summation order as k_fold2 (kern_misc.cu), so the result is bit-identical to the two-launch
-// step.  Z was written during this launch by other CTAs: L2-coherent loads (ld.global.cg), never
-// the non-coherent/L1 path.  T != nullptr: also the face traces of the new u (staged in sm).
-template <int NN>
-__device__ __forceinline__ void fold_element(const LevelDev &L, int e, const double *Z,
-                                             double *__restrict__ u, bool zero,
-                                             double *__restrict__ T, double *sm, const double *trs) {
-  constexpr int n = NN, n2 = n * n, n3 = n2 * n;
-  const long long Zs = L.Zs;
-  const int mx = L.m[0], my = L.m[1];
-  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
-  const int edim[3] = {L.nx, L.ny, L.nz};
-  int se[3][3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
-  const int nod[3] = {L.no[0], L.no[1], L.no[2]};
-  for (int t = threadIdx.x; t < n3; t += blockDim.x) {
-    const int i = t % n, j = (t / n) % n, k = t / n2;
-    const int idx[3] = {i, j, k};
-    bool v[3][3];
-    int wi[3][3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int no = nod[d], id = idx[d];
-      v[d][0] = id < no;        wi[d][0] = no + n + id;     // left-neighbour subdomain
-      v[d][1] = true;           wi[d][1] = no + id;         // own subdomain
-      v[d][2] = id >= n - no;   wi[d][2] = id - (n - no);   // right-neighbour subdomain
-    }
-    const long long g = (long long)e * n3 + t;
-    double du = zero ? 0.0 : u[g];
-#pragma unroll
-    for (int oz = 0; oz < 3; ++oz) {
-      if (!v[2][oz]) continue;
-      double z[9];
-#pragma unroll
-      for (int oy = 0; oy < 3; ++oy)
-#pragma unroll
-        for (int ox = 0; ox < 3; ++ox) {
-          const bool ok = v[0][ox] && v[1][oy];
-          const long long sidx = se[0][ox] + L.nx * (se[1][oy] + (long long)L.ny * se[2][oz]);
-          z[ox + 3 * oy] = ok ? __ldcg(Z + sidx * Zs + wi[0][ox] + mx * (wi[1][oy] + my * wi[2][oz])) : 0.0;
-        }
-#pragma unroll
-      for (int q = 0; q < 9; ++q) du += z[q];
-    }
-    u[g] = du;
-    if (T) sm[t] = du;
-  }
-  if (!T) return;
-  __syncthreads();
-  double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-#pragma unroll 4
-    for (int q = 0; q < n; ++q) {
-      const double vv = sm[base + q * stride];
-      rv += tr[q] * vv;
-      rder += tr[n + q] * vv;
-      lv += tr[2 * n + q] * vv;
-      lder += tr[3 * n + q] * vv;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
-}
-
-__device__ __forceinline__ unsigned atom_add_acqrel(unsigned *p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
-// index of the element at offset (q % 3 - 1, q / 3 % 3 - 1, q / 9 - 1) from e (periodic)
-__device__ __forceinline__ int nbr27(const LevelDev &L, int e, int q) {
-  const int ex = e % L.nx, ey = (e / L.nx) % L.ny, ez = e / (L.nx * L.ny);
-  const int x = wrap(ex + q % 3 - 1, L.nx), y = wrap(ey + (q / 3) % 3 - 1, L.ny), z = wrap(ez + q / 9 - 1, L.nz);
-  return x + L.nx * (y + L.ny * z);
-}
-
-struct FoldArgs {
-  unsigned *cnt;           // nullptr: no fused fold (Z is folded by a separate launch)
-  double *u;
-  double *T;               // traces of the new u (nullptr: not needed)
-  int zero;                // u = 0 on entry
-};
-
 // Shared memory: window X (S2 * M2, padded planes) | S_x, S_y, S_z | lam | W | gather offsets
-//                | trace table (12 NN) | ready list (32 ints)
-template <int M0, int M1, int M2, int NN, bool WIDE>
+template <int M0, int M1, int M2, bool WIDE>
 __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1, M2, WIDE>::MINB)
     k_fdm_eoc(LevelDev L, const double *__restrict__ r, double *__restrict__ Z, int color,
-              double *__restrict__ u, FoldArgs fa) {
+              double *__restrict__ u) {
   using SH = Shape<M0, M1, M2, WIDE>;
   constexpr int S2 = SH::S2, Mw = M0 * M1 * M2;
   extern __shared__ double sm[];
@@ -358,15 +260,12 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
   double *W0 = lam0 + M0 + M1 + M2;
   double *W[3] = {W0, W0 + M0, W0 + M0 + M1};
   long long *offs = reinterpret_cast<long long *>(W0 + M0 + M1 + M2);
-  double *trs = reinterpret_cast<double *>(offs + M0 + M1 + M2);
-  int *ready = reinterpret_cast<int *>(trs + 12 * NN);
   constexpr int mm[3] = {M0, M1, M2};
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     stage(Ss[d], L.S[d], mm[d] * mm[d]);
     stage(lam[d], L.lam[d], mm[d]);
     stage(W[d], L.W[d], mm[d]);
-    if (fa.T) stage(trs + d * 4 * NN, L.tr[d], 4 * NN);
   }
   int e = blockIdx.x;
   if (color >= 0) {       // subdomain bx of parity class `color` (2x2x2 colouring)
@@ -432,61 +331,8 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
     eoc_lines<0, SH, false, true>(X, Ss[0], wr);
   } else {
     const Blk G = {{M0, M1, M2}, {1, M0, M0 * M1}};   // global window order (Z)
-    EpiWeightStore ws{Z + (long long)e * L.Zs, G, {W[0], W[1], W[2]}};
+    EpiWeightStore ws{Z + (long long)e * Mw, G, {W[0], W[1], W[2]}};
     eoc_lines<0, SH, false, true>(X, Ss[0], ws);
-  }
-  if (fa.cnt) {
-    // publish this window, count it into the 27 elements it covers; the CTA whose count
-    // completes an element folds it (no spin-wait anywhere: the last arriver does the work)
-    __threadfence();
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) {
-      bool last = false;
-      int tgt = 0;
-      if (lane < 27) {
-        tgt = nbr27(L, e, lane);
-        last = atom_add_acqrel(fa.cnt + tgt, 1u) == 26u;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, last);
-      if (last) ready[__popc(bal & ((1u << lane) - 1u))] = tgt;
-      if (lane == 0) ready[31] = __popc(bal);
-    }
-    __syncthreads();
-    const int nready = ready[31];
-    for (int k = 0; k < nready; ++k) {
-      const int t = ready[k];
-      fold_element<NN>(L, t, Z, fa.u, fa.zero != 0, fa.T, X, trs);
-#ifndef PMG_NO_DISCARD
-      // consumer count of the 27 source windows just read; the last consumer drops the window's
-      // lines from L2 without writing them back (discard.global.L2): Z never reaches HBM
-      __threadfence();
-      __syncthreads();
-      if (warp == 0) {
-        bool drop = false;
-        int src = 0;
-        if (lane < 27) {
-          src = nbr27(L, t, lane);
-          drop = atom_add_acqrel(fa.cnt + L.Ne + src, 1u) == 26u;
-          if (drop) fa.cnt[L.Ne + src] = 0u;
-        }
-        if (lane == 0) fa.cnt[t] = 0u;
-        unsigned bal = __ballot_sync(0xffffffffu, drop);
-        while (bal) {
-          const int q = __ffs(bal) - 1;
-          bal &= bal - 1;
-          const int sw = __shfl_sync(0xffffffffu, src, q);
-          const char *zb = reinterpret_cast<const char *>(Z + (long long)sw * L.Zs);
-          const int lines = (L.Zs * 8) >> 7;
-          for (int li = lane; li < lines; li += 32)
-            asm volatile("discard.global.L2 [%0], 128;" ::"l"(zb + ((long long)li << 7)) : "memory");
-        }
-      }
-#else
-      if (threadIdx.x == 0) fa.cnt[t] = 0u;
-#endif
-      __syncthreads();
-    }
   }
 #ifdef PMG_PHASE_TIMING
   __syncthreads();
@@ -499,79 +345,54 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
 #undef PMG_PH
 }
 
-template <int M0, int M1, int M2, int NN>
+template <int M0, int M1, int M2>
 size_t eoc_smem() {
   return sizeof(double) * ((size_t)Shape<M0, M1, M2>::S2 * M2 + M0 * M0 + M1 * M1 + M2 * M2 +
-                           3 * (M0 + M1 + M2) + 12 * NN + 16);
+                           3 * (M0 + M1 + M2));
 }
 
-template <int M0, int M1, int M2, int NN, bool WIDE>
+template <int M0, int M1, int M2, bool WIDE>
 void eoc_launch_t(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
-                  const FoldArgs &fa, cudaStream_t s) {
-  const size_t sb = eoc_smem<M0, M1, M2, NN>();
+                  cudaStream_t s) {
+  const size_t sb = eoc_smem<M0, M1, M2>();
   static bool cfg = false;
   if (!cfg) {
     cfg = true;
-    cudaFuncSetAttribute(k_fdm_eoc<M0, M1, M2, NN, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_fdm_eoc<M0, M1, M2, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
-  k_fdm_eoc<M0, M1, M2, NN, WIDE><<<grid, Shape<M0, M1, M2, WIDE>::THREADS, sb, s>>>(L, r, Z, color, u, fa);
+  k_fdm_eoc<M0, M1, M2, WIDE><<<grid, Shape<M0, M1, M2, WIDE>::THREADS, sb, s>>>(L, r, Z, color, u);
 }
 
-template <int M0, int M1, int M2, int NN>
+template <int M0, int M1, int M2>
 void eoc_launch(const LevelDev &L, int grid, const double *r, double *Z, int color, double *u,
-                const FoldArgs &fa, cudaStream_t s) {
+                cudaStream_t s) {
   // one wave of 128-thread CTAs would leave the SMs mostly idle: widen the CTAs instead
   if (Shape<M0, M1, M2>::THREADS == 128 && grid <= 4 * num_sms())
-    eoc_launch_t<M0, M1, M2, NN, true>(L, grid, r, Z, color, u, fa, s);
+    eoc_launch_t<M0, M1, M2, true>(L, grid, r, Z, color, u, s);
   else
-    eoc_launch_t<M0, M1, M2, NN, false>(L, grid, r, Z, color, u, fa, s);
+    eoc_launch_t<M0, M1, M2, false>(L, grid, r, Z, color, u, s);
 }
 
 }  // namespace
 
-// Shapes of the benchmark configurations (c1-c5, all levels; window m_x, m_y, m_z and element
-// extent n); others use the generic kernels.
+// Shapes of the benchmark configurations (c1-c5, all levels); others use the generic kernels.
 #define PMG_EOC_SHAPES(X) \
-  X(23, 23, 23, 17) X(13, 13, 13, 9) X(7, 7, 7, 5) X(5, 5, 5, 3) X(11, 27, 27, 9) X(7, 15, 15, 5) \
-  X(5, 9, 9, 3)
+  X(23, 23, 23) X(13, 13, 13) X(7, 7, 7) X(5, 5, 5) X(11, 27, 27) X(7, 15, 15) X(5, 9, 9)
 
-static bool eoc_dispatch(const LevelDev &L, const double *r, double *Z, int color, double *u,
-                         const FoldArgs &fa, cudaStream_t s) {
+bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, double *u,
+                    cudaStream_t s) {
 #ifdef PMG_NO_EOC
   return false;
 #endif
   const int grid = color >= 0 ? L.Ne / 8 : L.Ne;
-#define PMG_EOC_CASE(a, b, c, nn)                                              \
-  if (L.m[0] == a && L.m[1] == b && L.m[2] == c && L.n == nn) {               \
-    eoc_launch<a, b, c, nn>(L, grid, r, Z, color, u, fa, s);                   \
-    return true;                                                              \
+#define PMG_EOC_CASE(a, b, c)                                    \
+  if (L.m[0] == a && L.m[1] == b && L.m[2] == c) {              \
+    eoc_launch<a, b, c>(L, grid, r, Z, color, u, s);            \
+    return true;                                                \
   }
   PMG_EOC_SHAPES(PMG_EOC_CASE)
 #undef PMG_EOC_CASE
   return false;
-}
-
-bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, double *u,
-                    cudaStream_t s) {
-  const FoldArgs none = {nullptr, nullptr, nullptr, 0};
-  return eoc_dispatch(L, r, Z, color, u, none, s);
-}
-
-bool fdm_fold_ok(int n, const int *m) {
-#ifdef PMG_NO_FUSED_FOLD
-  return false;
-#endif
-#define PMG_EOC_OK(a, b, c, nn) if (m[0] == a && m[1] == b && m[2] == c && n == nn) return true;
-  PMG_EOC_SHAPES(PMG_EOC_OK)
-#undef PMG_EOC_OK
-  return false;
-}
-
-cudaError_t launch_fdm_fold(const LevelDev &L, const double *r, double *Z, double *u, bool zero,
-                            double *T, unsigned *cnt, cudaStream_t s) {
-  const FoldArgs fa = {cnt, u, T, zero ? 1 : 0};
-  if (!cnt || !eoc_dispatch(L, r, Z, -1, nullptr, fa, s)) return cudaErrorInvalidValue;
-  return cudaGetLastError();
 }
 
 }  // namespace pmg

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__re
   const int n = NT > 0 ? NT : L.n;
   const int n3 = n * n * n;
   const int mx = L.m[0], my = L.m[1];
-  const long long Mw = L.Zs;
+  const long long Mw = L.Mw;
   const int e = blockIdx.x;
   const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
   const int edim[3] = {L.nx, L.ny, L.nz};

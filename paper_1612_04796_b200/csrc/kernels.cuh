@@ -19,8 +19,6 @@ struct LevelDev {
   const double *nodes;     // n reference nodes
   const double *Daug[3];   // [D | a ap b bp], n x (n+4) row-major (apply line GEMM)
   int Mw;                  // m0*m1*m2
-  int Zs;                  // stride of one subdomain's window in Z (Mw, or Mw padded to 16 doubles
-                           // = whole 128-byte lines for the fused Schwarz step's L2 discard)
   const double *Rz;        // eigen-divide table 1/(lam_x[p]+lam_y[q]+lam_z[o]) at [(p + m0 q) m2 + o]
 };
 
@@ -62,16 +60,6 @@ cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, c
 // compile-time-shape even/odd Schwarz kernel (kern_fdm_ct.cu); false if the shape is not built in
 bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, double *u,
                     cudaStream_t s);
-// Fused Schwarz step (kern_fdm_ct.cu): the subdomain solves AND the deterministic fold in one
-// launch.  Each CTA solves its subdomain, writes the weighted window to Z, and counts itself
-// into the 27 elements its window covers (cnt[]); the CTA that completes an element's count
-// folds that element (same fixed 27-source order as launch_fold) and emits its face traces.
-// Z pieces are consumed from L2 shortly after they are written and their lines are discarded
-// once all 27 consumers are done (cnt[Ne..2Ne) counts consumers), so Z does not round-trip
-// through HBM.  cnt: 2 Ne zero-initialised counters (left zero on exit).
-bool fdm_fold_ok(int n, const int *m);   // window shape m[3], element extent n
-cudaError_t launch_fdm_fold(const LevelDev &L, const double *r, double *Z, double *u, bool zero,
-                            double *T, unsigned *cnt, cudaStream_t s);
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s);
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)

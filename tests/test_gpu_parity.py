@@ -431,21 +431,3 @@ def test_ragged_grids_benchmark_shapes(name, ne):
         g.pmg_vcycle(ug, _t(f))
         uo = mg.vcycle(H, uo, f)
     assert _rel(_n(ug), uo) <= _tol(c.name)
-
-
-@pytest.mark.parametrize("name,ne", [("c1", None), ("c2", 3), ("c3", (3, 4, 3)), ("c5", (4, 3, 5))])
-def test_fused_fold_bitwise(name, ne):
-    """The fused Schwarz step (solve + last-arriver fold in one launch, Z consumed from L2) gives
-    bit-for-bit the two-launch result (same fixed 27-source summation order), cycle after cycle
-    (its element counters must return to zero at the end of every launch)."""
-    c = get_config(name, ne)
-    outs = []
-    for fused in (True, False):
-        g = _gpu(c)
-        g.set_fused_fold(fused)
-        f = _t(uniform_zero_mean(c.ndofs, 0))
-        u = torch.zeros_like(f)
-        for _ in range(3):
-            g.pmg_vcycle(u, f)
-        outs.append(_n(u))
-    assert np.array_equal(outs[0], outs[1])
