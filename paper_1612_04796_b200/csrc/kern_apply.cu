@@ -95,20 +95,13 @@ __global__ void k_apply(LevelDev L, const double *__restrict__ u, const double *
 // out = (E +- O)/2 is folded into A.
 // cmap: tile slot -> column p + n q (scripts/gen_colmap17.py): tiles whose base addresses are
 // spread over the 16 double banks, so the B loads and the C stores are conflict free.
-template <int DIR, bool FIRST>
-__device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
-                                           const double *__restrict__ Daug,
-                                           const unsigned short *cmap) {
-  constexpr int n = 17, n2 = n * n, H = 8, KA = n + 4;
-  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
-  constexpr int SO = DIR == 0 ? 1 : (DIR == 1 ? n : n2);
-  constexpr int SP = PD == 0 ? 1 : (PD == 1 ? n : n2);
-  constexpr int SQ = QD == 0 ? 1 : (QD == 1 ? n : n2);
-  constexpr int NCOL = n2, NT = (NCOL + 7) / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  // A fragments (row i = g for E and O; tail row 8 for E), K slot k = 4 ks + t
-  double aE[3], aO[3], at[3];
+// A fragments of the even/odd n = 17 line GEMM for lane (g, t): E rows, O rows, E tail row,
+// per K slice ks = 0..2 — built once per CTA into shared memory (eo17_afrag) so each pass loads
+// 9 values per lane instead of re-deriving them from Daug in global memory for every element.
+constexpr int EO17_AF = 9 * 32;     // doubles per direction
+__device__ __forceinline__ void eo17_afrag(const double *__restrict__ Daug, double *af) {
+  constexpr int n = 17, H = 8, KA = n + 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int ks = 0; ks < 3; ++ks) {
     const int k = ks * 4 + t;
@@ -121,12 +114,36 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
       return 0.0;
     };
     const double *r = Daug + g * KA;
-    aE[ks] = coefE(g);
-    at[ks] = coefE(H);
-    if (k < H) aO[ks] = 0.5 * (r[k] - r[n - 1 - k]);
-    else if (k == 9) aO[ks] = 0.5 * (r[n] - r[n + 2]);
-    else if (k == 10) aO[ks] = 0.5 * (r[n + 1] + r[n + 3]);
-    else aO[ks] = 0.0;
+    double aO;
+    if (k < H) aO = 0.5 * (r[k] - r[n - 1 - k]);
+    else if (k == 9) aO = 0.5 * (r[n] - r[n + 2]);
+    else if (k == 10) aO = 0.5 * (r[n + 1] + r[n + 3]);
+    else aO = 0.0;
+    af[(0 * 3 + ks) * 32 + lane] = coefE(g);
+    af[(1 * 3 + ks) * 32 + lane] = aO;
+    af[(2 * 3 + ks) * 32 + lane] = coefE(H);
+  }
+}
+
+template <int DIR, bool FIRST>
+__device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
+                                           const double *af, const unsigned short *cmap) {
+  constexpr int n = 17, n2 = n * n, H = 8;
+  constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
+  constexpr int SO = DIR == 0 ? 1 : (DIR == 1 ? n : n2);
+  constexpr int SP = PD == 0 ? 1 : (PD == 1 ? n : n2);
+  constexpr int SQ = QD == 0 ? 1 : (QD == 1 ? n : n2);
+  constexpr int NCOL = n2, NT = (NCOL + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  if (warp >= NT) return;
+  // A fragments (row i = g for E and O; tail row 8 for E), K slot k = 4 ks + t
+  double aE[3], aO[3], at[3];
+#pragma unroll
+  for (int ks = 0; ks < 3; ++ks) {
+    aE[ks] = af[(0 * 3 + ks) * 32 + lane];
+    aO[ks] = af[(1 * 3 + ks) * 32 + lane];
+    at[ks] = af[(2 * 3 + ks) * 32 + lane];
   }
   // B sources: lo / hi offsets, from U (k <= 8, 11) or from the face coefficients Cf (k = 9, 10)
   bool fromC[3];
@@ -139,13 +156,15 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     else if (k == 10) { o1[ks] = n2; o2[ks] = 3 * n2; }
     else { const int kk = k < H ? k : H; o1[ks] = kk * SO; o2[ks] = (n - 1 - kk) * SO; }
   }
-  for (int tile = warp; tile < NT; tile += nw) {
+  // one tile: B loads, 3 + 3 DMMAs (two accumulator chains), FMA tail row with a 2-step shuffle
+  auto compute = [&](int tile, double (&cE)[2], double (&cO)[2], double &tl, int &pb, int &qb) {
 #ifndef PMG_APPLY_NOCMAP
     const int nb = cmap[tile * 8 + g];
 #else
     const int nb = min(tile * 8 + g, NCOL - 1);
 #endif
-    const int qb = nb / n, pb = nb - qb * n;
+    qb = nb / n;
+    pb = nb - qb * n;
     const double *xb = U + pb * SP + qb * SQ;
     const double *cb = Cfd + pb + n * qb;
     double bE[3], bO[3];
@@ -156,18 +175,19 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
       bE[ks] = v1 + v2;
       bO[ks] = v1 - v2;
     }
-    double cE[2] = {0.0, 0.0}, cO[2] = {0.0, 0.0};
+    cE[0] = cE[1] = cO[0] = cO[1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) {
       dmma884(cE[0], cE[1], aE[ks], bE[ks]);
       dmma884(cO[0], cO[1], aO[ks], bO[ks]);
     }
-    double tl = 0.0;
+    tl = 0.0;
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) tl = fma(at[ks], bE[ks], tl);
     tl += __shfl_xor_sync(0xffffffffu, tl, 1);
     tl += __shfl_xor_sync(0xffffffffu, tl, 2);
-    __syncwarp();
+  };
+  auto epilogue = [&](int tile, const double (&cE)[2], const double (&cO)[2], double tl, int pb, int qb) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int slot = tile * 8 + 2 * t + j;
@@ -188,6 +208,24 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
       if (FIRST) *vb = tl;
       else *vb += tl;
     }
+  };
+  // software pipelined: the DMMAs of tile i + nw are issued before the epilogue of tile i
+  double cE0[2], cO0[2], cE1[2], cO1[2], tl0, tl1;
+  int pb0, qb0, pb1, qb1;
+  int tile = warp;
+  compute(tile, cE0, cO0, tl0, pb0, qb0);
+  for (;;) {
+    const int t1 = tile + nw;
+    if (t1 < NT) compute(t1, cE1, cO1, tl1, pb1, qb1);
+    __syncwarp();
+    epilogue(tile, cE0, cO0, tl0, pb0, qb0);
+    if (t1 >= NT) break;
+    const int t2 = t1 + nw;
+    if (t2 < NT) compute(t2, cE0, cO0, tl0, pb0, qb0);
+    __syncwarp();
+    epilogue(t1, cE1, cO1, tl1, pb1, qb1);
+    if (t2 >= NT) break;
+    tile = t2;
   }
 }
 
@@ -211,6 +249,7 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   double *Us = sm, *V = sm + n3 + 2, *Cf = V + n3, *ms = Cf + 12 * n2;
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(ms + 3 * n);
   unsigned short *cmap = reinterpret_cast<unsigned short *>(mbar + 1);      // n = 17 only
+  double *af17 = reinterpret_cast<double *>(cmap + ((PMG_COLMAP17_LEN + 3) & ~3));  // n = 17: 3 x EO17_AF
   const int edim[3] = {L.nx, L.ny, L.nz};
   const unsigned tbytes = 16u * n2;                                // 2 n^2 doubles per segment
   // Persistent: CTA b handles elements b, b + grid, ...  While element e is computed, the next
@@ -230,8 +269,11 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   };
   if (threadIdx.x == 0) mbar_init(mbar, 1);
   for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
-  if constexpr (NT == 17)
+  if constexpr (NT == 17) {
     for (int i = threadIdx.x; i < PMG_COLMAP17_LEN; i += blockDim.x) cmap[i] = kColMap17[i];
+    const int w = threadIdx.x >> 5;
+    if (w < 3) eo17_afrag(L.Daug[w], af17 + w * EO17_AF);
+  }
   __syncthreads();
   unsigned phase = 0;
 #ifdef PMG_PHASE_TIMING
@@ -299,10 +341,10 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
 #ifndef PMG_NO_APPLY_EO
     if constexpr (NT == 17) {            // even/odd passes (the transform stored -c4)
       PMG_APH(1);
-      apply_eo17<0, true>(U, Cf, V, L.Daug[0], cmap); __syncthreads();
+      apply_eo17<0, true>(U, Cf, V, af17, cmap); __syncthreads();
       PMG_APH(2);
-      apply_eo17<1, false>(U, Cf + 4 * n2, V, L.Daug[1], cmap); __syncthreads();
-      apply_eo17<2, false>(U, Cf + 8 * n2, V, L.Daug[2], cmap); __syncthreads();
+      apply_eo17<1, false>(U, Cf + 4 * n2, V, af17 + EO17_AF, cmap); __syncthreads();
+      apply_eo17<2, false>(U, Cf + 8 * n2, V, af17 + 2 * EO17_AF, cmap); __syncthreads();
       PMG_APH(3);
     } else
 #endif
@@ -457,7 +499,8 @@ bool apply_pipe_ok(const LevelDev &L) { return L.n == 3 || L.n == 5 || L.n == 9 
 
 static size_t apply_mma_smem(int n) {
   const size_t n2 = (size_t)n * n, n3 = n2 * n;
-  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2) + 2 * PMG_COLMAP17_LEN;
+  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2) + 2 * ((PMG_COLMAP17_LEN + 3) & ~3) +
+         (n == 17 ? sizeof(double) * 3 * EO17_AF : 0);
 }
 
 template <int NT, bool WIDE>

@@ -28,6 +28,8 @@ struct Shape {
   static constexpr int Hmax = (M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2)) / 2;
   static constexpr int THREADS = (Hmax >= 8 || WIDE) ? 256 : 128;
   static constexpr int MINB = Hmax >= 8 ? 2 : (WIDE ? 4 : 8);
+  static constexpr int NWS = THREADS / 32;                    // warps per subdomain
+  __device__ static __forceinline__ int wid() { return (int)(threadIdx.x >> 5); }
   template <int D> __host__ __device__ static constexpr int m() { return D == 0 ? M0 : (D == 1 ? M1 : M2); }
   template <int D> __host__ __device__ static constexpr int s() { return D == 0 ? 1 : (D == 1 ? M0 : S2); }
 };
@@ -40,8 +42,8 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
   constexpr int MP = SH::template m<PD>(), MQ = SH::template m<QD>();
   constexpr int SO = SH::template s<DIR>(), SP = SH::template s<PD>(), SQ = SH::template s<QD>();
   constexpr int NCOL = MP * MQ, NT = (NCOL + 7) / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = SH::THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = SH::wid();
+  constexpr int NW = SH::NWS;
   const int g = lane >> 2, t = lane & 3;
   if (warp >= NT) return;
   double aE[MT][KS], aO[MT][KS];
@@ -142,8 +144,8 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
   constexpr int MT = (H + 1 + 7) / 8, KS = (H + 1 + 3) / 4;
   constexpr int MP = SH::template m<0>(), MQ = SH::template m<1>();
   constexpr int SO = SH::S2, SQ = SH::template s<1>();
-  constexpr int NCOL = MP * MQ, NT = (NCOL + 7) / 8, NW = SH::THREADS / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NCOL = MP * MQ, NT = (NCOL + 7) / 8, NW = SH::NWS;
+  const int lane = threadIdx.x & 31, warp = SH::wid();
   const int g = lane >> 2, t = lane & 3;
   double aEf[MT][KS], aOf[MT][KS], aEb[MT][KS], aOb[MT][KS];
 #pragma unroll

@@ -95,6 +95,92 @@ __global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__re
   }
 }
 
+// Small elements (n = 3, 5): EPB elements per 256-thread CTA, one thread per DOF, same fixed
+// 27-source summation order as k_fold2; TR: the face traces of the new u from shared memory in
+// the same launch (a 27- or 125-DOF element left most of a 256-thread CTA idle, and the separate
+// trace launch cost as much as the fold).
+template <int NT, int EPB, bool TR>
+__global__ void __launch_bounds__(256) k_fold_small(LevelDev L, const double *__restrict__ Z,
+                                                  double *__restrict__ u, int zero,
+                                                  double *__restrict__ T) {
+  constexpr int n = NT, n2 = n * n, n3 = n2 * n;
+  __shared__ double sm[EPB * n3];
+  __shared__ double trs[12 * n];
+  const int mx = L.m[0], my = L.m[1];
+  const long long Zs = L.Mw;
+  const int le = threadIdx.x / n3, t = threadIdx.x - le * n3;
+  const int e = blockIdx.x * EPB + le;
+  if (TR)
+    for (int d = 0; d < 3; ++d)
+      for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) trs[d * 4 * n + i] = L.tr[d][i];
+  if (le < EPB && e < L.Ne) {
+    const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+    const int edim[3] = {L.nx, L.ny, L.nz};
+    int se[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int o = 0; o < 3; ++o) se[d][o] = wrap(ec[d] + o - 1, edim[d]);
+    const int i = t % n, j = (t / n) % n, k = t / n2;
+    const int idx[3] = {i, j, k};
+    const int nod[3] = {L.no[0], L.no[1], L.no[2]};
+    bool v[3][3];
+    int wi[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int no = nod[d], id = idx[d];
+      v[d][0] = id < no;        wi[d][0] = no + n + id;
+      v[d][1] = true;           wi[d][1] = no + id;
+      v[d][2] = id >= n - no;   wi[d][2] = id - (n - no);
+    }
+    const long long g = (long long)e * n3 + t;
+    double du = zero ? 0.0 : u[g];
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      if (!v[2][oz]) continue;
+      double z[9];
+#pragma unroll
+      for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          const bool ok = v[0][ox] && v[1][oy];
+          const long long sidx = se[0][ox] + L.nx * (se[1][oy] + (long long)L.ny * se[2][oz]);
+          z[ox + 3 * oy] = ok ? __ldg(Z + sidx * Zs + wi[0][ox] + mx * (wi[1][oy] + my * wi[2][oz])) : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) du += z[q];
+    }
+    u[g] = du;
+    if (TR) sm[le * n3 + t] = du;
+  }
+  if (!TR) return;
+  __syncthreads();
+  for (int w = threadIdx.x; w < EPB * 3 * n2; w += blockDim.x) {
+    const int lb = w / (3 * n2), r = w - lb * 3 * n2;
+    const int eb = blockIdx.x * EPB + lb;
+    if (eb >= L.Ne) break;
+    const int d = r / n2, p = r - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    const double *ue = sm + lb * n3;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+#pragma unroll
+    for (int q = 0; q < n; ++q) {
+      const double vv = ue[base + q * stride];
+      rv += tr[q] * vv;
+      rder += tr[n + q] * vv;
+      lv += tr[2 * n + q] * vv;
+      lder += tr[3 * n + q] * vv;
+    }
+    double *Td = T + (long long)eb * 12 * n2 + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Coarse level (P_0 = 1): u_0 = A_0^+ f_0 by global fast diagonalisation on the periodic
 // (2nx, 2ny, 2nz) grid with the constant mode removed (Alg. 1 l.295).
@@ -408,6 +494,19 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
 #define PMG_FOLD(NN)                                                                          \
   if (T) k_fold2<NN, true><<<L.Ne, 256, sb, s>>>(L, Z, u, z, T);                             \
   else k_fold2<NN, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
+  if (L.n == 3 || L.n == 5) {                 // several small elements per CTA, traces fused
+    const int z0 = zero ? 1 : 0;
+    if (L.n == 3) {
+      const int g = (L.Ne + 8) / 9;
+      if (T) k_fold_small<3, 9, true><<<g, 256, 0, s>>>(L, Z, u, z0, T);
+      else k_fold_small<3, 9, false><<<g, 256, 0, s>>>(L, Z, u, z0, nullptr);
+    } else {
+      const int g = (L.Ne + 1) / 2;
+      if (T) k_fold_small<5, 2, true><<<g, 256, 0, s>>>(L, Z, u, z0, T);
+      else k_fold_small<5, 2, false><<<g, 256, 0, s>>>(L, Z, u, z0, nullptr);
+    }
+    return cudaGetLastError();
+  }
   if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
     if (L.n == 33) k_fold2<33, false><<<dim3(L.Ne, 36), 256, 0, s>>>(L, Z, u, z, nullptr);
     else if (L.n == 5) k_fold2<5, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
