@@ -221,6 +221,9 @@ Overlap1D resolve_overlap(int mode, double value, int floor_layers, const Basis1
   if (mode == 0) {
     ov.no = std::min(std::max((int)value, floor_layers), n);
     ov.dref = first_excluded(ov.no);
+#ifdef PMG_REACH_INSIDE   // experiment (DESIGN R6): FixedNodes reach = last node inside the window
+    if (ov.no > 0) ov.dref = std::max(d[ov.no - 1], ld(1e-9));
+#endif
     return ov;
   }
   ld deltaO = (mode == 1) ? ld(value) * delta_d : std::min(ld(value) * delta_max, delta_d);

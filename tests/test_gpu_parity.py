@@ -17,12 +17,7 @@ from oracle.mf import MFHierarchy
 from oracle.dense import DenseHierarchy
 from oracle import mg
 
-TOL = 1e-11
-# c5 (element aspect ratio 48): kappa(A)*eps ~ 1e-10.  Two exact FP64 oracles (dense LU and
-# fast diagonalisation) already disagree by 7.4e-11 / 1.1e-10 after 1 / 2 cycles on c5's
-# element shape, so the iterate bar for this config is the
-# measured FP64 floor x ~4.  The apply and the residual check below stay at 1e-11.
-TOL_ANISO = 5e-10
+from tolerances import TOL, TOL_ANISO, TOL_ANISO_RES   # each bar's derivation is in tolerances.py
 
 
 def _tol(name):
@@ -117,22 +112,26 @@ def test_vcycle_parity(name, ne):
     f = uniform_zero_mean(c.ndofs, 0)
     u = np.zeros(c.ndofs)
     ug, fg = _t(u), _t(f)
-    # c5's plain V-cycle does not converge (rho > 1 after the first cycle; the paper uses it
-    # only inside CG for high aspect ratios), so round-off grows cycle by cycle: bar on cycle 1.
-    for k in range(1 if name == "c5" else 2):
+    # Two cycles everywhere except full-size c5, whose plain V-cycle diverges after the first
+    # (||r||/||r0|| = 0.17, 1.2, 9.8 for cycles 1-3; the paper runs it only inside CG for high
+    # aspect ratios): a divergent iteration amplifies the round-off of cycle 1 (GPU and oracle
+    # then differ by 8e-10 after cycle 2, scripts/c5_gap_probe.py), so that case stops at one.
+    for k in range(1 if (name == "c5" and ne is None) else 2):
         g.pmg_vcycle(ug, fg)
         u = mg.vcycle(H, u, f)
         assert _rel(_n(ug), u) <= _tol(name), k
-        # conditioning-insensitive check: the two iterates have the same residual to 1e-11
+        # conditioning-insensitive check: the two iterates have the same residual to TOL of
+        # ||f|| (c5: TOL_ANISO_RES, 5x the dense-vs-FDM oracle floor; tolerances.py)
         dr = H.apply(H.L, _n(ug) - u)
-        assert np.max(np.abs(dr)) <= (TOL if _tol(name) == TOL else 2e-10) * np.max(np.abs(f)), k
+        assert np.max(np.abs(dr)) <= (TOL if _tol(name) == TOL else TOL_ANISO_RES) * np.max(np.abs(f)), k
 
 
 def test_vcycle_parity_c3_full():
     test_vcycle_parity("c3", None)
 
 
-@pytest.mark.parametrize("name,ne,cycles", [("c1", None, 12), ("c2", None, 10), ("c4", 3, 6), ("c3", 4, 6)])
+@pytest.mark.parametrize("name,ne,cycles", [("c1", None, 12), ("c2", None, 10), ("c4", 3, 6), ("c3", 4, 6),
+                                             ("c3", None, 5), ("c4", None, 5)])
 def test_rate_per_cycle_three_digits(name, ne, cycles):
     c = get_config(name, ne)
     g = _gpu(c)
@@ -278,12 +277,16 @@ def _table1():
     return rows
 
 
-@pytest.mark.parametrize("row,P", [(1, 16), (1, 32), (7, 16), (7, 32), (2, 32), (8, 32)])
+@pytest.mark.parametrize("row,P", [(1, 16), (1, 32), (7, 16), (7, 32), (2, 32), (8, 32),
+                                   (3, 8), (3, 16), (4, 8), (4, 16), (9, 8), (9, 16), (10, 8), (10, 16),
+                                   (13, 8), (13, 16), (14, 8), (14, 16)])
 def test_table1_rates_at_paper_scale(row, P):
-    """The GPU (parity-pinned to the oracle) reproduces Table 1 at the paper's own grids for the
-    one-node-overlap rows (which do not depend on the unpinned hat-weight quintic, reading R6):
-    -lg rho within 0.06 of the printed value (paper protocol: random guess in [-1,1], RHS
-    M 3 sin x sin y sin z, iterate to 1e-10)."""
+    """The GPU (parity-pinned to the oracle) reproduces Table 1 at the paper's own grids: -lg rho
+    within 0.06 of the printed value (paper protocol: random guess in [-1,1], RHS
+    M 3 sin x sin y sin z, iterate to 1e-10; Table 1 :401-415).  Rows 3, 4, 9,
+    10, 13, 14 (relative overlaps) have window nodes inside the weight transition band, so they
+    pin the hat-weight reach of reading R6; rows 1, 2, 7, 8 (one node of overlap) pin the
+    operator, the transfers and the solver."""
     import math
     basis, solver, ov, paper = _table1()[row]
     from paper_1612_04796_b200 import DG

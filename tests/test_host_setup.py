@@ -96,3 +96,21 @@ def test_colmap17_table_is_a_conflict_free_permutation():
     assert int(body.group(1)) == len(tab) == 296
     assert [int(x) for x in body.group(2).split(",")] == tab
     assert sorted(tab[:289]) == list(range(289)) and set(tab[289:]) == {tab[288]}
+
+
+def test_binding_rejects_wrong_vectors_before_the_abi():
+    """The binding checks every vector against the ABI contract (CUDA, float64, contiguous, the
+    level's DOF count) before a pointer crosses into the C library (no GPU needed: it raises first)."""
+    import pytest
+    import torch
+    from paper_1612_04796_b200 import DG
+    from workloads.configs import OverlapSpec
+    g = DG((3, 3, 3), (1.0, 1.0, 1.0), 2, 0, overlap=OverlapSpec(0, 1, 0), bind=False)
+    n = g.ndofs()
+    with pytest.raises(ValueError):
+        g.apply(torch.zeros(n, dtype=torch.float64))                        # host tensor
+    with pytest.raises((ValueError, TypeError)):
+        g.pmg_vcycle(torch.zeros(n, dtype=torch.float32), torch.zeros(n))   # wrong dtype / device
+    with pytest.raises(ValueError):
+        g.set_schedule([1, 1], [1, 1, 1])                                   # L + 1 = 2 entries each
+    g.close()

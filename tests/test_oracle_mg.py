@@ -140,3 +140,38 @@ def test_mf_matches_dense_vcycle(cfg, ne):
     tol = 1e-12 if cfg != "c5" else 1e-8            # c5: cond(A_ss) ~ 1e6 (see test_oracle_schwarz)
     assert np.max(np.abs(a - b)) < tol * np.max(np.abs(a))
     assert np.max(np.abs(Hd.apply(Hd.L, a) - Hm.apply(Hm.L, a))) < 1e-11 * np.max(np.abs(Hd.apply(Hd.L, a)))
+
+
+def _table1_case(basis, ov, P, rows_want):
+    """Paper protocol: 2pi-periodic cube, N_e = (128/P)^3, seeded random
+    initial guess in [-1, 1], RHS M 3 sin x sin y sin z, V(1,1) to ||r_n|| <= 1e-10 ||r_0||,
+    -lg rho = -lg (r_n / r_0)^(1/n)."""
+    import math
+    from workloads import uniform_vector
+    from oracle.dense import mass_diag, node_coords
+    ne = 128 // P
+    L = 2 * math.pi
+    H = MFHierarchy((ne, ne, ne), (L, L, L), P, basis, 2.0, ov)
+    X, Y, Z = node_coords((ne, ne, ne), (L, L, L), P, basis)
+    b = mass_diag((ne, ne, ne), (L, L, L), P, basis) * 3 * np.sin(X) * np.sin(Y) * np.sin(Z)
+    b -= b.mean()
+    u = uniform_vector(H.ndofs(H.L), 3)
+    h = [mg.residual_norm(H, u, b)]
+    while h[-1] > 1e-10 * h[0] and len(h) < 40:
+        u = mg.vcycle(H, u, b)
+        h.append(mg.residual_norm(H, u, b))
+    return -math.log10((h[-1] / h[0]) ** (1.0 / (len(h) - 1)))
+
+
+@pytest.mark.parametrize("row,basis,ov,P,want", [
+    (3, GLL, OverlapSpec(1, 0.08, 0), 16, 2.13),     # PAPER.md:403 (Table 1 row 3)
+    (9, GL, OverlapSpec(1, 0.08, 0), 8, 1.15),       # PAPER.md:409 (row 9)
+    (13, GL, OverlapSpec(1, 0.09, 1), 8, 1.75),      # PAPER.md:413 (row 13)
+])
+def test_table1_relative_overlap_rows_pin_weight_reach(row, basis, ov, P, want):
+    """The hat-weight reach (reading R6: the transition ends at the first neighbour node outside
+    the window) is pinned by the convergence rates the paper prints for relative overlaps — rows
+    whose windows include nodes inside the transition band.  The geometric reach 2 delta_O/Delta
+    gave -lg rho 0.3-1.0 below these values; the oracle itself must land within 0.06."""
+    lg = _table1_case(basis, ov, P, want)
+    assert abs(lg - want) <= 0.06, (row, P, lg, want)
