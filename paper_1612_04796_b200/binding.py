@@ -163,17 +163,18 @@ class DG:
 
     def apply(self, u, level=None, out=None):
         level = self.L if level is None else level
-        out = self.empty(level) if out is None else out
         n = self.ndofs(level)
-        self._check(lib.dg_apply(self._c, level, _vec(u, n, "u"), _vec(out, n, "out"), _stream()))
+        pu = _vec(u, n, "u")
+        out = self.empty(level) if out is None else out
+        self._check(lib.dg_apply(self._c, level, pu, _vec(out, n, "out"), _stream()))
         return out
 
     def residual(self, u, f, level=None, out=None):
         level = self.L if level is None else level
-        out = self.empty(level) if out is None else out
         n = self.ndofs(level)
-        self._check(lib.dg_residual(self._c, level, _vec(u, n, "u"), _vec(f, n, "f"), _vec(out, n, "out"),
-                                    _stream()))
+        pu, pf = _vec(u, n, "u"), _vec(f, n, "f")
+        out = self.empty(level) if out is None else out
+        self._check(lib.dg_residual(self._c, level, pu, pf, _vec(out, n, "out"), _stream()))
         return out
 
     def schwarz_smooth(self, u, f, steps=1, level=None):
@@ -188,15 +189,16 @@ class DG:
         return uf
 
     def restrict(self, rf, level, out=None):
+        prf = _vec(rf, self.ndofs(level), "rf")
         out = self.empty(level - 1) if out is None else out
-        self._check(lib.dg_restrict(self._c, level, _vec(rf, self.ndofs(level), "rf"),
-                                    _vec(out, self.ndofs(level - 1), "out"), _stream()))
+        self._check(lib.dg_restrict(self._c, level, prf, _vec(out, self.ndofs(level - 1), "out"), _stream()))
         return out
 
     def coarse_solve(self, f0, out=None):
-        out = self.empty(0) if out is None else out
         n = self.ndofs(0)
-        self._check(lib.dg_coarse_solve(self._c, _vec(f0, n, "f0"), _vec(out, n, "out"), _stream()))
+        pf = _vec(f0, n, "f0")
+        out = self.empty(0) if out is None else out
+        self._check(lib.dg_coarse_solve(self._c, pf, _vec(out, n, "out"), _stream()))
         return out
 
     def set_schedule(self, nu1, nu2):
