@@ -124,7 +124,11 @@ int pmg_vcycle(dg_ctx *ctx, double *u, const double *f, void *stream);
 /* pcg_solve — inexact preconditioned CG (Golub-Ye) with one V-cycle
  * (zero initial guess) as preconditioner, until ||r||/||r_0|| <= rtol or maxit iterations.
  * u: initial guess in, solution out.  *iters receives the iteration count; res_hist (host,
- * maxit+1 doubles, or NULL) receives ||r_k||_2.  Synchronises `stream` once per iteration.
+ * maxit+1 doubles, or NULL) receives ||r_k||_2.  With graphs enabled (dg_set_graphs, default)
+ * and maxit < 8192 the whole solve is ONE CUDA-graph launch: the iteration is the body of a
+ * conditional WHILE node and the convergence test runs on the device, so `stream` is
+ * synchronised once per solve; otherwise (profiling, graphs off) once per iteration.  Both paths
+ * launch the same kernels in the same order (identical iterates).
  * Errors: PMG_EDIVERGED (non-finite scalar or ||r||/||r_0|| > 1e3), PMG_EMAXIT (u keeps the
  * last iterate). */
 int pcg_solve(dg_ctx *ctx, double *u, const double *f, double rtol, int maxit, int *iters,

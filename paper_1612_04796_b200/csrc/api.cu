@@ -72,6 +72,13 @@ struct dg_ctx {
   cudaStream_t cap_stream = nullptr;
   struct GraphEntry { double *u; const double *f; bool zero; cudaGraphExec_t exec; };
   std::vector<GraphEntry> graph_cache;
+  // whole PCG solves as one graph launch (conditional WHILE/IF nodes, device-side convergence test)
+  struct PcgGraph { double *u; const double *f; double rtol; int maxit; cudaGraphExec_t exec;
+                    long long lp, lw, li; };
+  std::vector<PcgGraph> pcg_cache;
+  cudaStream_t cap_stream2 = nullptr;
+  size_t o_hist = 0;          // PCG residual history (pmg::PMG_PCG_HIST doubles, device)
+  double *host_hist = nullptr;
   // optional per-kernel CUDA-event timing (dg_profile): slot = kind * 8 + level
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -81,6 +88,13 @@ struct dg_ctx {
 };
 
 namespace {
+
+void drop_graphs(dg_ctx *c) {
+  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
+  c->graph_cache.clear();
+  for (auto &g : c->pcg_cache) cudaGraphExecDestroy(g.exec);
+  c->pcg_cache.clear();
+}
 
 int fail(dg_ctx *c, int code, const std::string &msg) {
   if (c) c->err = msg;
@@ -200,6 +214,7 @@ void plan_workspace(dg_ctx *c) {
   c->o_prold = p.dbl(NL);
   c->o_part = p.dbl(2 * 2048);
   c->o_scal = p.dbl(64);
+  c->o_hist = p.dbl(pmg::PMG_PCG_HIST);
   c->ws_bytes = p.off + 256;
 }
 
@@ -593,8 +608,7 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
   if (!dev_ptr || bytes < c->ws_bytes || (reinterpret_cast<size_t>(dev_ptr) & 255))
     return fail(c, PMG_EWORKSPACE, "workspace too small or not 256-byte aligned");
   c->ws = static_cast<char *>(dev_ptr);
-  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);   // graphs baked the old workspace
-  c->graph_cache.clear();
+  drop_graphs(c);                                   // graphs baked the old workspace
   cudaStream_t s = S(stream);
   auto up = [&](size_t off, const std::vector<double> &v) -> cudaError_t {
     if (v.empty()) return cudaSuccess;
@@ -621,6 +635,7 @@ int dg_bind_workspace(dg_ctx *c, void *dev_ptr, size_t bytes, void *stream) {
     if (e == cudaSuccess) e = up(c->o_lam0[d], c->lam0[d]);
   }
   if (e == cudaSuccess && !c->host_pinned) e = cudaMallocHost(&c->host_pinned, 64 * sizeof(double));
+  if (e == cudaSuccess && !c->host_hist) e = cudaMallocHost(&c->host_hist, (pmg::PMG_PCG_HIST + 8) * sizeof(double));
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);   // host vectors must outlive the copies
   if (e != cudaSuccess) {
     c->ws = nullptr;
@@ -698,8 +713,7 @@ int dg_set_schedule(dg_ctx *c, const int *nu1, const int *nu2) {
   for (int l = 1; l <= c->L; ++l)
     if (nu1[l] < 0 || nu2[l] < 0) return fail(c, PMG_EINVAL, "negative smoothing count");
   for (int l = 0; l <= c->L; ++l) { c->nu1[l] = nu1[l]; c->nu2[l] = nu2[l]; }
-  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
-  c->graph_cache.clear();
+  drop_graphs(c);
   return PMG_OK;
 }
 
@@ -711,6 +725,115 @@ int pmg_vcycle(dg_ctx *c, double *u, const double *f, void *stream) {
   return vcycle_run(c, u, f, false, S(stream));
 }
 
+namespace {
+
+// Build the whole inexact PCG solve as one CUDA graph: prologue (r0, z0 = V(0,
+// r0), p0, <z0, r0>), then a conditional WHILE node whose body is one iteration (q = A p, alpha,
+// u/r update, ||r||, device-side convergence test k_pcg_check) followed by a conditional IF node
+// (z = V(0, r), Golub-Ye beta, p update) that runs only while the solve continues.  The kernels
+// and their order are those of the host-driven loop below, so the iterates are identical; the
+// host synchronises once per solve (to read the iteration count, status and history).
+int pcg_graph_build(dg_ctx *c, double *u, const double *f, double rtol, int maxit, dg_ctx::PcgGraph &out) {
+  const int L = c->L;
+  const long long N = c->lev[L].N;
+  double *r = wsp<double>(c, c->o_pr), *z = wsp<double>(c, c->o_pz), *p = wsp<double>(c, c->o_pp);
+  double *q = wsp<double>(c, c->o_pq), *rold = wsp<double>(c, c->o_prold);
+  double *part = wsp<double>(c, c->o_part), *scal = wsp<double>(c, c->o_scal);
+  double *hist = wsp<double>(c, c->o_hist);
+  cudaError_t e = cudaSuccess;
+  if (!c->cap_stream) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !c->cap_stream2) e = cudaStreamCreateWithFlags(&c->cap_stream2, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaStreamCreate");
+  cudaStream_t s = c->cap_stream, s2 = c->cap_stream2;
+  cudaGraph_t G = nullptr;
+  if ((e = cudaGraphCreate(&G, 0)) != cudaSuccess) return cuda_check(c, e, "cudaGraphCreate");
+  cudaGraphConditionalHandle hw, hi;
+  e = cudaGraphConditionalHandleCreate(&hw, G, 0, 0);
+  if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hi, G, 0, 0);
+  if (e != cudaSuccess) { cudaGraphDestroy(G); return cuda_check(c, e, "cudaGraphConditionalHandleCreate"); }
+  int st = PMG_OK;
+  auto add_cond = [&](cudaStream_t cs, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                      cudaGraph_t &body) -> cudaError_t {
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaError_t ee = cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &nd);
+    if (ee != cudaSuccess) return ee;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((ee = cudaGraphAddNode(&node, cg, deps, nd, &np)) != cudaSuccess) return ee;
+    body = np.conditional.phGraph_out[0];
+    return cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies);
+  };
+  const long long l0 = c->launches;
+  cudaGraph_t wbody = nullptr, ibody = nullptr;
+  // prologue
+  e = cudaStreamBeginCaptureToGraph(s, G, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    st = residual_impl(c, L, u, f, r, s);                                        // r0 = f - A u0
+    if (!st) st = pmg::launch_dot(r, r, N, part, scal + 2, s) ? PMG_ECUDA : PMG_OK;
+    if (!st) st = pmg::launch_pcg_start(scal, hist, maxit, hw, s) ? PMG_ECUDA : PMG_OK;
+    if (!st) st = vcycle_impl(c, z, r, true, s);                                 // z0 = V(0, r0)
+    if (!st) st = pmg::launch_copy(p, z, N, s) ? PMG_ECUDA : PMG_OK;             // p0 = z0
+    if (!st) st = pmg::launch_zr_beta(z, r, r, N, part, scal, true, s) ? PMG_ECUDA : PMG_OK;
+    c->launches += 4;
+    if (!st) e = add_cond(s, hw, cudaGraphCondTypeWhile, wbody);
+    cudaGraph_t G2 = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(s, &G2);
+    if (e == cudaSuccess) e = e2;
+  }
+  out.lp = c->launches - l0;
+  // while body: one iteration up to the convergence test, then the IF node
+  if (!st && e == cudaSuccess) {
+    const long long l1 = c->launches;
+    e = cudaStreamBeginCaptureToGraph(s2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      st = residual_impl(c, L, p, nullptr, q, s2);                               // q = A p
+      if (!st) st = pmg::launch_pq_alpha(p, q, N, part, scal, s2) ? PMG_ECUDA : PMG_OK;
+      if (!st) st = pmg::launch_cg_update(u, r, rold, p, q, N, part, scal, s2) ? PMG_ECUDA : PMG_OK;
+      if (!st) st = pmg::launch_pcg_check(scal, hist, rtol, maxit, hw, hi, s2) ? PMG_ECUDA : PMG_OK;
+      c->launches += 3;
+      if (!st) e = add_cond(s2, hi, cudaGraphCondTypeIf, ibody);
+      cudaGraph_t W2 = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(s2, &W2);
+      if (e == cudaSuccess) e = e2;
+    }
+    out.lw = c->launches - l1;
+  }
+  if (!st && e == cudaSuccess) {
+    const long long l2 = c->launches;
+    e = cudaStreamBeginCaptureToGraph(s2, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      st = vcycle_impl(c, z, r, true, s2);                                       // z = V(0, r)
+      if (!st) st = pmg::launch_zr_beta(z, r, rold, N, part, scal, false, s2) ? PMG_ECUDA : PMG_OK;
+      if (!st) st = pmg::launch_p_update(p, z, N, scal, s2) ? PMG_ECUDA : PMG_OK;  // p = z + beta p
+      c->launches += 2;
+      cudaGraph_t I2 = nullptr;
+      cudaError_t e2 = cudaStreamEndCapture(s2, &I2);
+      if (e == cudaSuccess) e = e2;
+    }
+    out.li = c->launches - l2;
+  }
+  c->launches = l0;
+  if (st || e != cudaSuccess) {
+    cudaGraphDestroy(G);
+    return st ? st : cuda_check(c, e, "pcg graph capture");
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, G, 0);
+  cudaGraphDestroy(G);
+  if (e != cudaSuccess) return cuda_check(c, e, "cudaGraphInstantiate (pcg)");
+  out.u = u; out.f = f; out.rtol = rtol; out.maxit = maxit; out.exec = exec;
+  return PMG_OK;
+}
+
+}  // namespace
+
 int pcg_solve(dg_ctx *c, double *u, const double *f, double rtol, int maxit, int *iters,
               double *res_hist, void *stream) {
   int st = check_level(c, c ? c->L : 0);
@@ -718,6 +841,34 @@ int pcg_solve(dg_ctx *c, double *u, const double *f, double rtol, int maxit, int
   if (!c->schwarz_ready) return fail(c, PMG_ESTATE, "dg_schwarz_setup not called");
   if (!u || !f || maxit < 0) return fail(c, PMG_EINVAL, "pcg_solve: bad arguments");
   cudaStream_t s = S(stream);
+  if (c->graphs && !c->prof && maxit < pmg::PMG_PCG_HIST) {
+    const dg_ctx::PcgGraph *pg = nullptr;
+    for (auto &g : c->pcg_cache)
+      if (g.u == u && g.f == f && g.rtol == rtol && g.maxit == maxit) pg = &g;
+    if (!pg) {
+      dg_ctx::PcgGraph ng;
+      if ((st = pcg_graph_build(c, u, f, rtol, maxit, ng))) return st;
+      c->pcg_cache.push_back(ng);
+      pg = &c->pcg_cache.back();
+    }
+    double *scal = wsp<double>(c, c->o_scal), *hist = wsp<double>(c, c->o_hist);
+    cudaError_t e = cudaGraphLaunch(pg->exec, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c->host_pinned, scal + 30, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_check(c, e, "pcg_solve (graph)");
+    const int k = (int)c->host_pinned[1];
+    const int status = (int)c->host_pinned[2];
+    c->launches += pg->lp + (long long)k * pg->lw + (long long)std::max(k - 1, 0) * pg->li;
+    if (iters) *iters = k;
+    if (res_hist) {
+      e = cudaMemcpy(c->host_hist, hist, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_check(c, e, "pcg_solve history");
+      std::memcpy(res_hist, c->host_hist, sizeof(double) * (k + 1));
+    }
+    if (status == PMG_EDIVERGED) return fail(c, PMG_EDIVERGED, k == 0 ? "non-finite initial residual" : "PCG diverged");
+    if (status == PMG_EMAXIT) return fail(c, PMG_EMAXIT, "PCG reached maxit");
+    return PMG_OK;
+  }
   const int L = c->L;
   const long long N = c->lev[L].N;
   double *r = wsp<double>(c, c->o_pr), *z = wsp<double>(c, c->o_pz), *p = wsp<double>(c, c->o_pp);
@@ -803,8 +954,7 @@ long long dg_launch_count(const dg_ctx *c) { return c ? c->launches : -1; }
 int dg_set_colored(dg_ctx *c, int enable) {
   if (!c) return PMG_EINVAL;
   c->colored = enable != 0;
-  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
-  c->graph_cache.clear();
+  drop_graphs(c);
   return PMG_OK;
 }
 
@@ -845,8 +995,10 @@ void dg_destroy(dg_ctx *c) {
   if (!c) return;
   if (c->host_pinned) cudaFreeHost(c->host_pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-  for (auto &g : c->graph_cache) cudaGraphExecDestroy(g.exec);
+  drop_graphs(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->cap_stream2) cudaStreamDestroy(c->cap_stream2);
+  if (c->host_hist) cudaFreeHost(c->host_hist);
   delete c;
 }
 

@@ -458,6 +458,35 @@ __global__ void k_p_update(double *__restrict__ p, const double *__restrict__ z,
     p[g] = z[g] + beta * p[g];
 }
 
+// Device-side control of the graph-driven PCG (same tests as the host loop:
+// diverged = non-finite or ||r|| > 1e3 ||r_0||, converged = ||r|| <= rtol ||r_0||, else maxit).
+// Status codes mirror include/pmg_dg.h (PMG_EDIVERGED = 6, PMG_EMAXIT = 7); -1 = running.
+__global__ void k_pcg_start(double *scal, double *hist, int maxit, cudaGraphConditionalHandle hw) {
+  const double r0 = sqrt(scal[2]);
+  scal[30] = r0;
+  scal[31] = 0.0;
+  hist[0] = r0;
+  const int status = !isfinite(r0) ? 6 : (r0 == 0.0 ? 0 : (maxit == 0 ? 7 : -1));
+  scal[32] = status;
+  cudaGraphSetConditional(hw, status == -1 ? 1u : 0u);
+}
+
+__global__ void k_pcg_check(double *scal, double *hist, double rtol, int maxit,
+                            cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+  const double rn = sqrt(scal[2]), r0 = scal[30];
+  const int k = (int)scal[31] + 1;
+  scal[31] = k;
+  hist[k] = rn;
+  int status = -1;
+  if (!isfinite(rn) || rn > 1e3 * r0) status = 6;
+  else if (rn <= rtol * r0) status = 0;
+  else if (k >= maxit) status = 7;
+  scal[32] = status;
+  const unsigned cont = status == -1 ? 1u : 0u;
+  cudaGraphSetConditional(hw, cont);
+  cudaGraphSetConditional(hi, cont);
+}
+
 // b = M * amp * sin(kx x) sin(ky y) sin(kz z) at the nodes (diagonal quadrature)
 __global__ void k_rhs_sin(LevelDev L, double dx, double dy, double dz, double amp, double kx,
                           double ky, double kz, double *__restrict__ b) {
@@ -637,6 +666,16 @@ cudaError_t launch_zr_beta(const double *z, const double *r, const double *rold,
 cudaError_t launch_p_update(double *p, const double *z, long long N, const double *scal,
                             cudaStream_t s) {
   k_p_update<<<grid_for(N, 256), 256, 0, s>>>(p, z, N, scal);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_start(double *scal, double *hist, int maxit, cudaGraphConditionalHandle hw,
+                             cudaStream_t s) {
+  k_pcg_start<<<1, 1, 0, s>>>(scal, hist, maxit, hw);
+  return cudaGetLastError();
+}
+cudaError_t launch_pcg_check(double *scal, double *hist, double rtol, int maxit,
+                             cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi, cudaStream_t s) {
+  k_pcg_check<<<1, 1, 0, s>>>(scal, hist, rtol, maxit, hw, hi);
   return cudaGetLastError();
 }
 cudaError_t launch_rhs_sin(const LevelDev &L, double dx, double dy, double dz, double amp,

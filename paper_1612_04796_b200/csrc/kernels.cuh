@@ -103,6 +103,13 @@ cudaError_t launch_zr_beta(const double *z, const double *r, const double *rold,
                            double *partial, double *scal, bool first, cudaStream_t s);
 cudaError_t launch_p_update(double *p, const double *z, long long N, const double *scal,
                             cudaStream_t s);
+// device-side PCG control (graph path of pcg_solve): scal[30] = ||r_0||, scal[31] = k,
+// scal[32] = status (0 converged / PMG_EDIVERGED / PMG_EMAXIT / -1 running); hist[k] = ||r_k||.
+constexpr int PMG_PCG_HIST = 8192;
+cudaError_t launch_pcg_start(double *scal, double *hist, int maxit, cudaGraphConditionalHandle hw,
+                             cudaStream_t s);
+cudaError_t launch_pcg_check(double *scal, double *hist, double rtol, int maxit,
+                             cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi, cudaStream_t s);
 cudaError_t launch_rhs_sin(const LevelDev &L, double dx, double dy, double dz, double amp,
                            double kx, double ky, double kz, double *b, cudaStream_t s);
 

@@ -434,3 +434,26 @@ def test_ragged_grids_benchmark_shapes(name, ne):
         g.pmg_vcycle(ug, _t(f))
         uo = mg.vcycle(H, uo, f)
     assert _rel(_n(ug), uo) <= _tol(c.name)
+
+
+@pytest.mark.parametrize("name,ne", [("c5", 3), ("c2", 3), ("c1", None)])
+def test_pcg_graph_equals_host_loop(name, ne):
+    """pcg_solve as one CUDA-graph launch (conditional WHILE/IF nodes, device-side convergence
+    test) gives the host-driven loop's iterates and residual history bit for bit."""
+    c = get_config(name, ne)
+    out = []
+    for graphs in (True, False):
+        g = _gpu(c)
+        g.set_graphs(graphs)
+        f = _t(uniform_zero_mean(c.ndofs, 0))
+        u = torch.zeros_like(f)
+        _, hist, ok = g.pcg_solve(u, f, rtol=1e-10, maxit=200)
+        assert ok
+        out.append((_n(u), np.array(hist)))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    # a solve that hits maxit reports PMG_EMAXIT through the graph path too
+    g = _gpu(c)
+    u = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
+    _, hist, ok = g.pcg_solve(u, _t(uniform_zero_mean(c.ndofs, 0)), rtol=1e-14, maxit=3)
+    assert not ok and len(hist) == 4
