@@ -495,7 +495,14 @@ static size_t apply_pipe_smem(int n) {
   return sizeof(double) * (3 * n3 + 24 * n2 + 3 * n);
 }
 
-bool apply_pipe_ok(const LevelDev &L) { return L.n == 3 || L.n == 5 || L.n == 9 || L.n == 17; }
+// PMG_FORCE_DFMA (diagnostic A/B build, scripts/gpu_dfma_ab.sh): levels with n <= 9 use the scalar
+// FP64-FMA kernels (k_apply, k_fdm) instead of the DMMA line GEMMs.
+bool apply_pipe_ok(const LevelDev &L) {
+#ifdef PMG_FORCE_DFMA
+  if (L.n <= 9) return false;
+#endif
+  return L.n == 3 || L.n == 5 || L.n == 9 || L.n == 17;
+}
 
 static size_t apply_mma_smem(int n) {
   const size_t n2 = (size_t)n * n, n3 = n2 * n;
@@ -554,6 +561,12 @@ cudaError_t launch_apply(const LevelDev &L, const double *u, const double *T, co
                          double *out, cudaStream_t s) {
   const int n = L.n;
 
+#ifdef PMG_FORCE_DFMA
+  if (n <= 9) {
+    k_apply<<<L.Ne, 256, 0, s>>>(L, u, T, f, out);
+    return cudaGetLastError();
+  }
+#endif
   if (n <= 17) {
     return launch_apply_pipe(L, u, T, f, out, nullptr, 0, nullptr, s);
   } else {

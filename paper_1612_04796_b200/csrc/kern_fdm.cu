@@ -525,6 +525,9 @@ cudaError_t launch_fdm_colored(const LevelDev &L, const double *r, double *u, cu
 
 cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *scr, bool smem,
                        size_t smem_bytes, cudaStream_t s) {
+#ifdef PMG_FORCE_DFMA
+  if (L.n > 9) {
+#endif
   if (fdm_eoc_launch(L, r, Z, -1, nullptr, s)) return cudaGetLastError();   // compile-time shape
   if (fdm_mma_ok(L)) {
     configure_smem();
@@ -541,6 +544,9 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
     else k_fdm_mma<8><<<L.Ne, FDM_BIG_THREADS, sb, s>>>(L, r, Z, -1, nullptr);
     return cudaGetLastError();
   }
+#ifdef PMG_FORCE_DFMA
+  }
+#endif
   if (smem) {
     static size_t configured = 0;
     if (smem_bytes > configured) {

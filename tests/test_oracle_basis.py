@@ -82,3 +82,16 @@ def test_interpolation_reproduces_polynomials(basis):
 def test_penalty_examples():
     for P, D, exp in _golden("penalty_examples.txt"):
         assert math.isclose(penalty_min(int(P), float(D)), float(exp), rel_tol=1e-14)
+
+
+def test_c1_penalty_is_spec_definition():
+    """BASELINE c1 runs "penalty mu as defined in SPEC.md": mu = 2 penalty_min(P, Delta) with
+    penalty_min = P(P+1)/Delta — 160 at P = 4, Delta = 1/4.
+    The oracle's operator must assemble exactly that mu from c1's penalty factor."""
+    from oracle.basis import penalty_min, stability_threshold
+    from workloads import get_config
+    c = get_config("c1")
+    delta = c.length[0] / c.ne[0]
+    mu = c.penalty * stability_threshold(c.P, delta)
+    assert abs(mu - 2 * penalty_min(c.P, delta)) <= 1e-12 * mu
+    assert abs(mu - 160.0) <= 1e-12

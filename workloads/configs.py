@@ -4,7 +4,10 @@ Overlap choices follow SURVEY.md §8(c) C-8 (recorded in DESIGN.md):
   c1 FixedNodes(1); c2 GL Relative(0.09)+floor 1 (Table 1 row 13, PAPER.md:414);
   c3, c4 GLL Relative(0.08) (Table 1 row 3, PAPER.md:403);
   c5 MaxRelative(0.08)+floor 1 (Table 2 "0.08 max").
-Penalty factor 2 for all.
+Penalty (the ABI's `penalty` is the factor on the coercivity threshold P(P+1)/(2 Delta), reading
+R2): factor 2 = the paper's "mu = 2 mu_min" with mu_min the stability threshold
+for c2-c5; c1 states "penalty mu as defined in SPEC.md", i.e. 2 x the printed example
+P(P+1)/Delta, which is factor 4 here.
 """
 from dataclasses import dataclass, field
 import math
@@ -48,7 +51,7 @@ TWO_PI = 2.0 * math.pi
 
 CONFIGS = {
     "c1": Config("c1", (4, 4, 4), (1.0, 1.0, 1.0), 4, GLL, OverlapSpec(OVL_NODES, 1, 0),
-                 run="vcycle", cycles=1),
+                 penalty=4.0, run="vcycle", cycles=1),        # mu = 2 P(P+1)/Delta
     "c2": Config("c2", (8, 8, 8), (TWO_PI, TWO_PI, TWO_PI), 8, GL, OverlapSpec(OVL_REL, 0.09, 1),
                  rhs="sin", run="solve", cycles=30),
     "c3": Config("c3", (16, 16, 16), (1.0, 1.0, 1.0), 16, GLL, OverlapSpec(OVL_REL, 0.08, 0),
