@@ -261,7 +261,10 @@ int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *ou
   pmg::LevelDev d = level_dev(c, l);
   double *T = wsp<double>(c, c->lev[l].o_T);
   if (!have_traces) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
-  if (c->lev[l].o_cb) {
+  if (c->lev[l].o_cb && pmg::apply33_ok(d)) {
+    LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply33(d, u, T, f, out, wsp<double>(c, c->lev[l].o_v), s));
+    c->launches += 1;
+  } else if (c->lev[l].o_cb) {
     LAUNCHK(c, K_APPLY, l, s, pmg::launch_apply_global(d, u, T, f, out, wsp<double>(c, c->lev[l].o_cb),
                                                        wsp<double>(c, c->lev[l].o_v), s));
     c->launches += 4;

@@ -43,6 +43,11 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
 cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
                                 double *out, double *Cb, double *V, cudaStream_t s);
 bool fdm_mma_ok(const LevelDev &L);
+// P = 32 (n = 33) apply / residual: two slab kernels with even/odd DMMA line GEMMs in shared
+// memory (kern_apply33.cu); V: Ne * 33^3 scratch (x + z contributions)
+bool apply33_ok(const LevelDev &L);
+cudaError_t launch_apply33(const LevelDev &L, const double *u, const double *T, const double *f,
+                           double *out, double *V, cudaStream_t s);
 // p-transfers as batched global line GEMMs (n_f > 17); X1, X2: Ne * nf * nf * nc doubles each
 cudaError_t launch_restrict_global(const LevelDev &Lf, int nc, const double *I, const double *rf,
                                    double *fc, double *X1, double *X2, cudaStream_t s);
