@@ -301,7 +301,10 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
       if (emit) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
       continue;
     }
-    if (h.fdm_path == 1) {
+    if (h.fdm_path == 1 && pmg::fdm45_ok(d)) {
+      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm45(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
+      c->launches += 2;
+    } else if (h.fdm_path == 1) {
       LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_global(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
       c->launches += 6;
     } else {

@@ -22,11 +22,11 @@ __host__ __device__ constexpr int plane_stride(int m0, int m1) {
 
 // WIDE: 256 threads for small windows too — used when the whole grid fits in one wave (small
 // meshes, e.g. c2's 512 subdomains), where a CTA's latency, not the SM's throughput, sets the time.
-template <int M0, int M1, int M2, bool WIDE = false>
+template <int M0, int M1, int M2, bool WIDE = false, int TH = 0>
 struct Shape {
   static constexpr int S2 = plane_stride(M0, M1);
   static constexpr int Hmax = (M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2)) / 2;
-  static constexpr int THREADS = (Hmax >= 8 || WIDE) ? 256 : 128;
+  static constexpr int THREADS = TH ? TH : ((Hmax >= 8 || WIDE) ? 256 : 128);
   static constexpr int MINB = Hmax >= 8 ? 2 : (WIDE ? 4 : 8);
   static constexpr int NWS = THREADS / 32;                    // warps per subdomain
   __device__ static __forceinline__ int wid() { return (int)(threadIdx.x >> 5); }
@@ -375,6 +375,132 @@ void eoc_launch(const LevelDev &L, int grid, const double *r, double *Z, int col
     eoc_launch_t<M0, M1, M2, false>(L, grid, r, Z, color, u, s);
 }
 
+// ---- P = 32 windows (m = 45, 729 KB: larger than an SM's shared memory) --------------------
+// Three slab kernels over two L2-resident window buffers (Ne x 45^3 each, c4: 47 MB):
+//   k_fdm45_a  (subdomain, z-slab of ZS planes): gather the slab of the window, forward x and y
+//              passes (plane-local), slab -> W1;
+//   k_fdm45_b  (subdomain, y-slab of YS lines): forward z with the eigen-divide epilogue, backward
+//              z (z columns are complete in a y-slab), slab -> W2;
+//   k_fdm45_c  (subdomain, z-slab): backward y and x, weighted store to Z (window order).
+// The even/odd line GEMMs (eoc_lines, 2 x 3 x 6 DMMAs per 8-column tile) run on the slab in
+// shared memory; 128-thread CTAs (the m = 45 A fragments alone are 36 doubles per lane).
+constexpr int W45 = 45, ZS45 = 5, YS45 = 5, NS45 = W45 / ZS45;
+using SZ45 = Shape<W45, W45, ZS45, false, 128>;     // z-slab block
+using SY45 = Shape<W45, YS45, W45, false, 128>;     // y-slab block
+
+__global__ void __launch_bounds__(128, 3) k_fdm45_a(LevelDev L, const double *__restrict__ r,
+                                                    double *__restrict__ W1) {
+  extern __shared__ double sm[];
+  constexpr int S2 = SZ45::S2;
+  double *X = sm, *Sx = X + S2 * ZS45, *Sy = Sx + W45 * W45;
+  long long *offs = reinterpret_cast<long long *>(Sy + W45 * W45);
+  const int e = blockIdx.y, z0 = blockIdx.x * ZS45;
+  stage(Sx, L.S[0], W45 * W45);
+  stage(Sy, L.S[1], W45 * W45);
+  fdm_offsets(L, e, offs);
+  __syncthreads();
+  const long long *xo = offs, *yo = offs + W45, *zo = offs + 2 * W45 + z0;
+  for (int w = threadIdx.x; w < W45 * W45 * ZS45; w += blockDim.x) {
+    const int bc = w / W45, a = w - bc * W45;
+    const int c = bc / W45, b = bc - c * W45;
+    cp_async8(X + a + W45 * b + S2 * c, r + xo[a] + yo[b] + zo[c]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const Blk B = {{W45, W45, ZS45}, {1, W45, S2}};
+  EpiStore st{X, B};
+  eoc_lines<0, SZ45, true, true>(X, Sx, st); __syncthreads();
+  eoc_lines<1, SZ45, true, true>(X, Sy, st); __syncthreads();
+  double *out = W1 + (long long)e * L.Mw + (long long)z0 * W45 * W45;
+  for (int w = threadIdx.x; w < W45 * W45 * ZS45; w += blockDim.x) {
+    const int c = w / (W45 * W45), ab = w - c * W45 * W45;
+    out[w] = X[ab + S2 * c];
+  }
+}
+
+__global__ void __launch_bounds__(128, 3) k_fdm45_b(LevelDev L, const double *__restrict__ W1,
+                                                    double *__restrict__ W2) {
+  extern __shared__ double sm[];
+  constexpr int S2 = SY45::S2;
+  double *X = sm, *Sz = X + S2 * W45;
+  const int e = blockIdx.y, y0 = blockIdx.x * YS45;
+  stage(Sz, L.S[2], W45 * W45);
+  const double *in = W1 + (long long)e * L.Mw + (long long)y0 * W45;
+  for (int w = threadIdx.x; w < W45 * YS45 * W45; w += blockDim.x) {     // (a, b, c): rows of 45
+    const int bc = w / W45, a = w - bc * W45;
+    const int c = bc / YS45, b = bc - c * YS45;
+    cp_async8(X + a + W45 * b + S2 * c, in + a + W45 * b + W45 * W45 * c);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const Blk B = {{W45, YS45, W45}, {1, W45, S2}};
+  EpiDivide dv{X, B, {L.lam[0], L.lam[1] + y0, L.lam[2]}};
+  EpiStore st{X, B};
+  eoc_lines<2, SY45, true, false>(X, Sz, dv); __syncthreads();
+  eoc_lines<2, SY45, false, false>(X, Sz, st); __syncthreads();
+  double *out = W2 + (long long)e * L.Mw + (long long)y0 * W45;
+  for (int w = threadIdx.x; w < W45 * YS45 * W45; w += blockDim.x) {
+    const int bc = w / W45, a = w - bc * W45;
+    const int c = bc / YS45, b = bc - c * YS45;
+    out[a + W45 * b + W45 * W45 * c] = X[a + W45 * b + S2 * c];
+  }
+}
+
+__global__ void __launch_bounds__(128, 3) k_fdm45_c(LevelDev L, const double *__restrict__ W2,
+                                                    double *__restrict__ Z) {
+  extern __shared__ double sm[];
+  constexpr int S2 = SZ45::S2;
+  double *X = sm, *Sx = X + S2 * ZS45, *Sy = Sx + W45 * W45, *Wt = Sy + W45 * W45;
+  const int e = blockIdx.y, z0 = blockIdx.x * ZS45;
+  stage(Sx, L.S[0], W45 * W45);
+  stage(Sy, L.S[1], W45 * W45);
+  stage(Wt, L.W[0], W45);
+  stage(Wt + W45, L.W[1], W45);
+  stage(Wt + 2 * W45, L.W[2] + z0, ZS45);
+  const double *in = W2 + (long long)e * L.Mw + (long long)z0 * W45 * W45;
+  for (int w = threadIdx.x; w < W45 * W45 * ZS45; w += blockDim.x) {
+    const int c = w / (W45 * W45), ab = w - c * W45 * W45;
+    cp_async8(X + ab + S2 * c, in + w);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const Blk B = {{W45, W45, ZS45}, {1, W45, S2}};
+  EpiStore st{X, B};
+  eoc_lines<1, SZ45, false, true>(X, Sy, st); __syncthreads();
+  const Blk G = {{W45, W45, ZS45}, {1, W45, W45 * W45}};             // global window order
+  EpiWeightStore ws{Z + (long long)e * L.Mw + (long long)z0 * W45 * W45, G, {Wt, Wt + W45, Wt + 2 * W45}};
+  eoc_lines<0, SZ45, false, true>(X, Sx, ws);
+}
+
+}  // namespace
+
+bool fdm45_ok(const LevelDev &L) {
+#ifdef PMG_NO_FDM45
+  return false;
+#endif
+  return L.m[0] == W45 && L.m[1] == W45 && L.m[2] == W45 && L.n == 33;
+}
+
+// W1, W2: Ne * 45^3 scratch each (L2-resident window buffers)
+cudaError_t launch_fdm45(const LevelDev &L, const double *r, double *W1, double *W2, double *Z,
+                         cudaStream_t s) {
+  const size_t sa = sizeof(double) * ((size_t)SZ45::S2 * ZS45 + 2 * W45 * W45 + 3 * W45);
+  const size_t sb = sizeof(double) * ((size_t)SY45::S2 * W45 + W45 * W45);
+  const size_t sc = sizeof(double) * ((size_t)SZ45::S2 * ZS45 + 2 * W45 * W45 + 3 * W45);
+  static bool cfg = false;
+  if (!cfg) {
+    cfg = true;
+    cudaFuncSetAttribute(k_fdm45_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
+    cudaFuncSetAttribute(k_fdm45_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    cudaFuncSetAttribute(k_fdm45_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+  }
+  k_fdm45_a<<<dim3(NS45, L.Ne), 128, sa, s>>>(L, r, W1);
+  k_fdm45_b<<<dim3(W45 / YS45, L.Ne), 128, sb, s>>>(L, W1, W2);
+  k_fdm45_c<<<dim3(NS45, L.Ne), 128, sc, s>>>(L, W2, Z);
+  return cudaGetLastError();
+}
+
+namespace {
 }  // namespace
 
 // Shapes of the benchmark configurations (c1-c5, all levels); others use the generic kernels.

@@ -46,6 +46,10 @@ bool fdm_mma_ok(const LevelDev &L);
 // P = 32 (n = 33) apply / residual: two slab kernels with even/odd DMMA line GEMMs in shared
 // memory (kern_apply33.cu); V: Ne * 33^3 scratch (x + z contributions)
 bool apply33_ok(const LevelDev &L);
+// P = 32 Schwarz solve on 45^3 windows: three slab kernels (kern_fdm_ct.cu); W1, W2: Ne * 45^3
+bool fdm45_ok(const LevelDev &L);
+cudaError_t launch_fdm45(const LevelDev &L, const double *r, double *W1, double *W2, double *Z,
+                         cudaStream_t s);
 cudaError_t launch_apply33(const LevelDev &L, const double *u, const double *T, const double *f,
                            double *out, double *V, cudaStream_t s);
 // p-transfers as batched global line GEMMs (n_f > 17); X1, X2: Ne * nf * nf * nc doubles each
