@@ -457,3 +457,28 @@ def test_pcg_graph_equals_host_loop(name, ne):
     u = torch.zeros(c.ndofs, dtype=torch.float64, device="cuda")
     _, hist, ok = g.pcg_solve(u, _t(uniform_zero_mean(c.ndofs, 0)), rtol=1e-14, maxit=3)
     assert not ok and len(hist) == 4
+
+
+@pytest.mark.parametrize("basis,P,k", [(0, 2, 6), (1, 2, 6), (0, 4, 4), (1, 4, 4)])
+def test_gpu_convergence_order(basis, P, k):
+    """NEXT row f4: the GPU solve of A u = M 3 sin x sin y sin z converges to u = sin x sin y sin z
+    at O(h^{P+1}) under mesh refinement k^3 -> (2k)^3 (north_star), same bounds
+    as the oracle's own CPU pin (test_oracle_operator.test_convergence_order)."""
+    import math
+    from oracle.dense import node_coords
+    from oracle.dense import mass_diag
+    errs = []
+    for kk in (k, 2 * k):
+        c = Config("order", (kk, kk, kk), (2 * math.pi,) * 3, P, basis, OverlapSpec(1, 0.09, 1))
+        g = _gpu(c)
+        f = g.rhs_sin(3.0, 1.0, 1.0, 1.0)
+        u = torch.zeros_like(f)
+        _, hist, ok = g.pcg_solve(u, f, rtol=1e-13, maxit=80)
+        assert ok
+        X, Y, Z = node_coords(c.ne, c.length, c.P, c.basis)
+        M = mass_diag(c.ne, c.length, c.P, c.basis)
+        err = _n(u) - np.sin(X) * np.sin(Y) * np.sin(Z)
+        err -= np.sum(M * err) / np.sum(M)
+        errs.append(math.sqrt(np.sum(M * err * err)))
+    order = math.log2(errs[0] / errs[1])
+    assert P + 0.75 <= order <= P + 2.25, (order, errs)
