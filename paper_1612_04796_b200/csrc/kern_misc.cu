@@ -95,6 +95,132 @@ __global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__re
   }
 }
 
+// Row fold (Eq. 10): a warp folds whole x-rows of the element.  Lane a of a
+// row is the window x-index a in [0, m_x): lanes n_o <= a < n_o + n read the row of a window
+// centred on this element column (own x), lanes a >= n_o + n read the same row of the LEFT
+// neighbour's window (its right overlap covers DOFs i = a - n_o - n) and lanes a < n_o that of
+// the RIGHT neighbour's — one load instruction fetches all three x-sources of a row, two
+// shuffles bring the strip values to the DOFs they cover.  The (y, z) sources are row-uniform:
+// with 2 n_o <= n (MERGED) a row has the own window plus at most one neighbour per direction
+// (4 predicated loads), otherwise all 3 x 3 combinations are tested (9).  Every address is
+// computed once per row instead of once per DOF and source (the register fold k_fold2 spent 303
+// thread instructions per DOF, 27 mostly predicated-off loads), and RB rows per warp are in
+// flight at once.  32 / m_x rows share a warp when they fit (n = 9: two rows of 13 lanes).
+// Fixed summation order -> deterministic.  TR: face traces of the new u from shared memory.
+template <int NT, bool TR, bool MERGED>
+__global__ void __launch_bounds__(256, 4) k_fold4(LevelDev L, const double *__restrict__ Z,
+                                                  double *__restrict__ u, int zero,
+                                                  double *__restrict__ T) {
+  extern __shared__ double sm[];          // TR: the folded element (n^3) + trace table (12 n)
+  const int n = NT > 0 ? NT : L.n;
+  const int n2 = n * n, n3 = n2 * n;
+  const int mx = L.m[0], my = L.m[1];
+  const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
+  const long long Mw = L.Mw;
+  const int e = blockIdx.x;
+  const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+  const int edim[3] = {L.nx, L.ny, L.nz};
+  // all offsets are 32-bit element indices into Z (the launcher checks Ne * Mw < 2^31)
+  int sb[3][3];                       // source-subdomain base per direction and offset -1, 0, +1
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+      sb[d][o] = wrap(ec[d] + o - 1, edim[d]) * (int)(d == 0 ? Mw : (d == 1 ? Mw * L.nx : Mw * L.nx * L.ny));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int rpw = 32 / mx;                                  // rows per warp instruction (>= 1)
+  const int sr = lane / mx, a = lane - sr * mx;
+  const bool act = sr < rpw;
+  const int ox = a < no0 ? 2 : (a < no0 + n ? 1 : 0);       // right nb | own | left nb window
+  const int i = a - no0;
+  const bool own = act && ox == 1;
+  const bool addL = own && i < no0, addR = own && i >= n - no0;
+  const int srcL = min(lane + n, 31), srcR = max(lane - n, 0);
+  const int wsy = mx, wsz = mx * my;
+  // per-source offsets: own / left / right window in y and z, x part folded into the own-y term
+  const int xb = (ox == 0 ? sb[0][0] : (ox == 1 ? sb[0][1] : sb[0][2])) + a;
+  const int yO = sb[1][1] + wsy * no1 + xb, yL = sb[1][0] + wsy * (no1 + n) + xb, yR = sb[1][2] - wsy * (n - no1) + xb;
+  const int zO = sb[2][1] + wsz * no2, zL = sb[2][0] + wsz * (no2 + n), zR = sb[2][2] - wsz * (n - no2);
+  double *ue = u + (long long)e * n3 + i;
+  constexpr int RB = MERGED ? 4 : 2, NL = MERGED ? 4 : 9;
+  const int rstep = nw * rpw;
+  for (int rb = warp * rpw + sr; rb < n2 + sr; rb += rstep * RB) {
+    double z[RB][NL], uo[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int row = rb + q * rstep;
+      const bool rv = act && row < n2;
+      const int k = row / n, j = row - k * n;
+      uo[q] = (rv && own && !zero) ? ue[n * row] : 0.0;
+      const int yj = wsy * j, zk = wsz * k;
+      if (MERGED) {
+        const bool ly = j < no1, lz = k < no2;
+        const bool py = ly || j >= n - no1, pz = lz || k >= n - no2;
+        const int y0 = yO + yj, y1 = (ly ? yL : yR) + yj;
+        const int z0 = zO + zk, z1 = (lz ? zL : zR) + zk;
+        z[q][0] = rv ? __ldg(Z + (y0 + z0)) : 0.0;
+        z[q][1] = (rv && py) ? __ldg(Z + (y1 + z0)) : 0.0;
+        z[q][2] = (rv && pz) ? __ldg(Z + (y0 + z1)) : 0.0;
+        z[q][3] = (rv && py && pz) ? __ldg(Z + (y1 + z1)) : 0.0;
+      } else {
+#pragma unroll
+        for (int oz = 0; oz < 3; ++oz) {
+          const bool pz = oz == 1 || (oz == 0 ? k < no2 : k >= n - no2);
+          const int zo = (oz == 0 ? zL : (oz == 1 ? zO : zR)) + zk;
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy) {
+            const bool py = oy == 1 || (oy == 0 ? j < no1 : j >= n - no1);
+            const int yo = (oy == 0 ? yL : (oy == 1 ? yO : yR)) + yj;
+            z[q][oy + 3 * oz] = (rv && py && pz) ? __ldg(Z + (yo + zo)) : 0.0;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int row = rb + q * rstep;
+      double v = z[q][0];
+#pragma unroll
+      for (int c = 1; c < NL; ++c) v += z[q][c];
+      const double vl = __shfl_sync(0xffffffffu, v, srcL), vr = __shfl_sync(0xffffffffu, v, srcR);
+      double res = uo[q] + v;
+      if (addL) res += vl;
+      if (addR) res += vr;
+      if (own && row < n2) {
+        ue[n * row] = res;
+        if (TR) sm[i + n * row] = res;
+      }
+    }
+  }
+  if (!TR) return;
+  __syncthreads();
+  // fused trace pass of the following residual: face values / derivatives of the new u
+  double *trs = sm + n3;
+  for (int d = 0; d < 3; ++d)
+    for (int t = threadIdx.x; t < 4 * n; t += blockDim.x) trs[d * 4 * n + t] = L.tr[d][t];
+  __syncthreads();
+  double *Te = T + (long long)e * 12 * n2;
+  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
+    const int d = t / n2, p = t - d * n2;
+    const int p0 = p % n, p1 = p / n;
+    int base, stride;
+    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
+    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+    else { base = p0 + n * p1; stride = n2; }
+    const double *tr = trs + d * 4 * n;
+    double lv = 0, lder = 0, rv = 0, rder = 0;
+    for (int q = 0; q < n; ++q) {
+      const double v = sm[base + q * stride];
+      rv += tr[q] * v;
+      rder += tr[n + q] * v;
+      lv += tr[2 * n + q] * v;
+      lder += tr[3 * n + q] * v;
+    }
+    double *Td = Te + d * 4 * n2;
+    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+  }
+}
+
 // Small elements (n = 3, 5): EPB elements per 256-thread CTA, one thread per DOF, same fixed
 // 27-source summation order as k_fold2; TR: the face traces of the new u from shared memory in
 // the same launch (a 27- or 125-DOF element left most of a 256-thread CTA idle, and the separate
@@ -536,6 +662,32 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
     }
     return cudaGetLastError();
   }
+#ifndef PMG_FOLD2
+  if (L.m[0] <= 32 && L.n >= 9 && sizeof(double) * ((size_t)L.n * L.n * L.n + 12 * L.n) <= 160 * 1024 &&
+      (long long)L.Ne * L.Mw < (1LL << 31)) {
+    // row fold (k_fold4): window rows fit a warp, the element fits shared memory for the traces
+    const int n = L.n;
+    const bool merged = 2 * L.no[0] <= n && 2 * L.no[1] <= n && 2 * L.no[2] <= n;
+    const size_t sb4 = T ? sizeof(double) * ((size_t)n * n * n + 12 * n) : 0;
+#define PMG_FOLD4(NN, MM)                                                                       \
+  do {                                                                                          \
+    static bool cfg4 = false;                                                                   \
+    if (!cfg4) {                                                                                \
+      cfg4 = true;                                                                              \
+      cudaFuncSetAttribute(k_fold4<NN, true, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    }                                                                                           \
+    if (T) k_fold4<NN, true, MM><<<L.Ne, 256, sb4, s>>>(L, Z, u, z, T);                         \
+    else k_fold4<NN, false, MM><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);                      \
+  } while (0)
+    if (n == 17 && merged) PMG_FOLD4(17, true);
+    else if (n == 9 && merged) PMG_FOLD4(9, true);
+    else if (n == 9) PMG_FOLD4(9, false);
+    else if (merged) PMG_FOLD4(0, true);
+    else PMG_FOLD4(0, false);
+#undef PMG_FOLD4
+    return cudaGetLastError();
+  }
+#endif
   if (T && (sb > 200 * 1024 || L.n < 9)) {   // n = 33: no room; n < 9: separate kernels are faster
     if (L.n == 33) k_fold2<33, false><<<dim3(L.Ne, 36), 256, 0, s>>>(L, Z, u, z, nullptr);
     else if (L.n == 5) k_fold2<5, false><<<L.Ne, 256, 0, s>>>(L, Z, u, z, nullptr);
