@@ -327,6 +327,10 @@ int coarse_impl(dg_ctx *c, const double *f0, double *u0, cudaStream_t s) {
     LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_one(d0, C, f0, u0, s));
     return PMG_OK;
   }
+  if (pmg::coarse_cluster_ok(C)) {
+    LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_cluster(d0, C, f0, u0, s));
+    return PMG_OK;
+  }
   if (c->G[2] <= 32) {
     LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_fused(d0, C, f0, G1, G2, u0, s));
     c->launches += 4;   // launch_coarse_fused issues 5 kernels

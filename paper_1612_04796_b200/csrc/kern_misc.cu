@@ -2,7 +2,11 @@
 // arXiv:1612.04796; PAPER.md line numbers cited per kernel.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "kcommon.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pmg {
 namespace {
@@ -476,6 +480,106 @@ __global__ void __launch_bounds__(1024) k_coarse_one(CoarseDev C, int nx, int ny
   }
 }
 
+// Whole coarse solve in ONE thread-block cluster (8 CTAs, distributed shared memory) for coarse
+// grids beyond one CTA's reach (1024 < G_x G_y G_z <= 32^3: c2/c5 16^3, c3 32^3).  CTA r keeps
+// the z-planes [r pp, (r+1) pp) of the lexicographic grid in its shared memory: the x and y
+// passes are plane-local; for the z pass (forward S_z^T, eigen-divide, backward S_z) the columns
+// are dealt out over the cluster and a warp reads / writes its column's G_z values straight from
+// the owning CTAs' shared memory (DSMEM), lane = z index, values exchanged by shuffles as in
+// k_coarse_z.  One launch instead of five, no global scratch; Alg. 1 l.295.
+__global__ void __launch_bounds__(512) k_coarse_cluster(CoarseDev C, int nx, int ny,
+                                                        const double *__restrict__ f0,
+                                                        double *__restrict__ u0) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+  const int Gx = C.G[0], Gy = C.G[1], Gz = C.G[2];
+  const int plane = Gx * Gy;
+  const int pp = (Gz + CS - 1) / CS;
+  const int z0 = rk * pp, nzl = max(0, min(Gz, z0 + pp) - z0);
+  extern __shared__ double sm[];
+  double *A = sm, *B = sm + pp * plane;
+  double *Sx = B + pp * plane, *Sy = Sx + Gx * Gx, *Sz = Sy + Gy * Gy;
+  double *SxT = Sz + Gz * Gz, *SzT = SxT + Gx * Gx;        // transposed copies: the backward x and z
+  double *lx = SzT + Gz * Gz, *ly = lx + Gx, *lz = ly + Gy;  // passes read S rows lane-contiguously
+  for (int i = threadIdx.x; i < Gx * Gx; i += blockDim.x) {
+    const double v = C.S[0][i];
+    Sx[i] = v;
+    SxT[(i % Gx) * Gx + i / Gx] = v;
+  }
+  for (int i = threadIdx.x; i < Gy * Gy; i += blockDim.x) Sy[i] = C.S[1][i];
+  for (int i = threadIdx.x; i < Gz * Gz; i += blockDim.x) {
+    const double v = C.S[2][i];
+    Sz[i] = v;
+    SzT[(i % Gz) * Gz + i / Gz] = v;
+  }
+  for (int i = threadIdx.x; i < Gx; i += blockDim.x) lx[i] = C.lam[0][i];
+  for (int i = threadIdx.x; i < Gy; i += blockDim.x) ly[i] = C.lam[1][i];
+  for (int i = threadIdx.x; i < Gz; i += blockDim.x) lz[i] = C.lam[2][i];
+  const int nl = nzl * plane;
+  for (int g = threadIdx.x; g < nl; g += blockDim.x) {
+    const int X = g % Gx, Y = (g / Gx) % Gy, zl = g / plane;
+    A[g] = __ldg(f0 + coarse_elem_index(nx, ny, X, Y, z0 + zl));
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < nl; g += blockDim.x) {            // x forward: B = S_x^T A
+    const int o = g % Gx;
+    const double *row = A + (g - o);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += Sx[k * Gx + o] * row[k];
+    B[g] = acc;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < nl; g += blockDim.x) {            // y forward: A = S_y^T B
+    const int a = g % Gx, o = (g / Gx) % Gy, zl = g / plane;
+    const double *col = B + a + plane * zl;
+    double acc = 0;
+    for (int k = 0; k < Gy; ++k) acc += Sy[k * Gy + o] * col[k * Gx];
+    A[g] = acc;
+  }
+  cl.sync();
+  {   // z forward, divide (null mode -> 0), z backward on this CTA's share of the columns
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int cpc = (plane + CS - 1) / CS;
+    const int c1 = min(plane, (rk + 1) * cpc);
+    double *RA = cl.map_shared_rank(A, min(lane / pp, CS - 1));
+    const int zoff = plane * (lane % pp);
+    const bool zl = lane < Gz;
+    for (int cidx = rk * cpc + warp; cidx < c1; cidx += nw) {
+      const int a = cidx % Gx, b = cidx / Gx;
+      const double v = zl ? RA[cidx + zoff] : 0.0;
+      double acc = 0.0;
+      for (int k = 0; k < Gz; ++k) {
+        const double vk = __shfl_sync(0xffffffffu, v, k);
+        if (zl) acc += Sz[k * Gz + lane] * vk;
+      }
+      double w = 0.0;
+      if (zl && !(a == 0 && b == 0 && lane == 0)) w = acc / (lx[a] + ly[b] + lz[lane]);
+      double out = 0.0;
+      for (int k = 0; k < Gz; ++k) {
+        const double wk = __shfl_sync(0xffffffffu, w, k);
+        if (zl) out += SzT[k * Gz + lane] * wk;
+      }
+      if (zl) RA[cidx + zoff] = out;
+    }
+  }
+  cl.sync();
+  for (int g = threadIdx.x; g < nl; g += blockDim.x) {            // y backward: B = S_y A
+    const int a = g % Gx, Y = (g / Gx) % Gy, zl = g / plane;
+    const double *col = A + a + plane * zl;
+    double acc = 0;
+    for (int k = 0; k < Gy; ++k) acc += Sy[Y * Gy + k] * col[k * Gx];
+    B[g] = acc;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < nl; g += blockDim.x) {            // x backward -> u_0 (element-major)
+    const int X = g % Gx, Y = (g / Gx) % Gy, zl = g / plane;
+    const double *row = B + (g - X);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += SxT[k * Gx + X] * row[k];
+    u0[coarse_elem_index(nx, ny, X, Y, z0 + zl)] = acc;
+  }
+}
+
 // x-backward pass writing u_0 in element-major order
 __global__ void k_coarse_xb(CoarseDev C, int nx, int ny, const double *__restrict__ G,
                             double *__restrict__ u0) {
@@ -739,6 +843,42 @@ cudaError_t launch_coarse_one(const LevelDev &L0, const CoarseDev &C, const doub
   }
   k_coarse_one<<<1, 1024, sb, s>>>(C, L0.nx, L0.ny, f0, u0);
   return cudaGetLastError();
+}
+
+bool coarse_cluster_ok(const CoarseDev &C) {
+#ifdef PMG_NO_COARSE_CLUSTER
+  return false;
+#endif
+  // measured: 16^3 (c2) 36 -> 17 us per solve; at 32^3 (c3, c5) eight SMs are LSU-bound (72 us
+  // against 66 us for the five-launch path over the whole GPU), so the cluster serves N_0 <= 8192
+  return C.G[0] <= 32 && C.G[1] <= 32 && C.G[2] <= 32 && C.G[2] >= 8 &&
+         (long long)C.G[0] * C.G[1] * C.G[2] <= 8192;
+}
+
+cudaError_t launch_coarse_cluster(const LevelDev &L0, const CoarseDev &C, const double *f0,
+                                  double *u0, cudaStream_t s) {
+  constexpr int CS = 8;
+  const int plane = C.G[0] * C.G[1], pp = (C.G[2] + CS - 1) / CS;
+  const size_t sb = sizeof(double) * (2 * (size_t)pp * plane + 2 * C.G[0] * C.G[0] + C.G[1] * C.G[1] +
+                                      2 * C.G[2] * C.G[2] + C.G[0] + C.G[1] + C.G[2]);
+  static bool cfg = false;
+  if (!cfg) {
+    cfg = true;
+    cudaFuncSetAttribute(k_coarse_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(CS);
+  lc.blockDim = dim3(512);
+  lc.dynamicSmemBytes = sb;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, k_coarse_cluster, C, L0.nx, L0.ny, f0, u0);
 }
 
 cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const double *f0,

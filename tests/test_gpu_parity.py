@@ -387,6 +387,19 @@ def test_vector_helpers_and_coarse_at_c3_size():
     assert _rel(_n(g.coarse_solve(_t(f0))), H.coarse(f0)) <= TOL
 
 
+@pytest.mark.parametrize("ne,length", [((6, 5, 7), (1.0, 1.0, 1.0)), ((16, 4, 9), (3.0, 1.0, 2.0)),
+                                       ((5, 6, 16), (1.0, 2.0, 1.0)), ((8, 8, 8), (1.0, 1.0, 1.0))])
+def test_coarse_cluster_ragged(ne, length):
+    """Coarse pseudo-inverse (Alg. 1 l.295) on the one-cluster path with non-cubic grids whose
+    z extent does not divide evenly over the 8 CTAs (G_z = 14, 18, 32; some CTAs own no plane),
+    and on c2's 16^3 grid."""
+    c = Config("coarse", ne, length, 2, 0, OverlapSpec(0, 1, 0))
+    g = _gpu(c)
+    H = _oracle(c)
+    f0 = uniform_vector(H.ndofs(0), 11)
+    assert _rel(_n(g.coarse_solve(_t(f0))), H.coarse(f0)) <= TOL
+
+
 def test_single_level_hierarchy_p2():
     """P = 2: one smoothing level above the P = 1 coarse level (L = 1)."""
     c = Config("p2", (4, 4, 4), (1.0, 1.0, 1.0), 2, 1, OverlapSpec(1, 0.5, 0))
