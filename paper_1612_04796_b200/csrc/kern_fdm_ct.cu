@@ -71,13 +71,26 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
       off1[ks] = min(k, H) * SO; off2[ks] = (H + 1 + min(k, H - 1)) * SO;
     }
   }
-  auto colpq = [](int n, int &p, int &q) {
-    if (QF) { p = n / MQ; q = n - p * MQ; } else { q = n / MP; p = n - q * MP; }
+  // Column bookkeeping without per-tile divisions: a lane tracks (p, q) of its B column and of
+  // its two C columns and steps them by the 8 NW columns between its tiles (the div/mod by a
+  // constant cost ~15 integer instructions per column and tile in 16-bit emulation).
+  struct Col { int p, q; };
+  auto col_init = [](int n, Col &c) {
+    if (QF) { c.p = n / MQ; c.q = n - c.p * MQ; } else { c.q = n / MP; c.p = n - c.q * MP; }
   };
-  auto compute = [&](int tile, double (&cE)[MT][2], double (&cO)[MT][2]) {
-    int pb, qb;
-    colpq(min(tile * 8 + g, NCOL - 1), pb, qb);
-    const double *xb = X + pb * SP + qb * SQ;
+  constexpr int STEP = 8 * NW;
+  auto col_adv = [](Col &c) {
+    if (QF) { c.q += STEP % MQ; c.p += STEP / MQ; if (c.q >= MQ) { c.q -= MQ; ++c.p; } }
+    else { c.p += STEP % MP; c.q += STEP / MP; if (c.p >= MP) { c.p -= MP; ++c.q; } }
+  };
+  auto col_ok = [](const Col &c) { return QF ? c.p < MP : c.q < MQ; };
+  Col cb, c0, c1;
+  col_init(warp * 8 + g, cb);
+  col_init(warp * 8 + 2 * t, c0);
+  col_init(warp * 8 + 2 * t + 1, c1);
+  auto compute = [&](double (&cE)[MT][2], double (&cO)[MT][2]) {
+    const double *xb = X + (col_ok(cb) ? cb.p * SP + cb.q * SQ : (MP - 1) * SP + (MQ - 1) * SQ);
+    col_adv(cb);
     double bE[KS], bO[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -95,13 +108,12 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
         dmma884(cO[mt][0], cO[mt][1], aO[mt][ks], bO[ks]);
       }
   };
-  auto epilogue = [&](int tile, const double (&cE)[MT][2], const double (&cO)[MT][2]) {
+  auto epilogue = [&](const double (&cE)[MT][2], const double (&cO)[MT][2]) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int n = tile * 8 + 2 * t + j;
-      if (n >= NCOL) continue;
-      int p, q;
-      colpq(n, p, q);
+      const Col c = j ? c1 : c0;
+      if (!col_ok(c)) continue;
+      const int p = c.p, q = c.q;
       const double cf = epi.template col<DIR>(p, q);
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -117,20 +129,22 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
         }
       }
     }
+    col_adv(c0);
+    col_adv(c1);
   };
   double cE0[MT][2], cO0[MT][2], cE1[MT][2], cO1[MT][2];
   int tile = warp;
-  compute(tile, cE0, cO0);
+  compute(cE0, cO0);
   for (;;) {
     const int t1 = tile + NW;
-    if (t1 < NT) compute(t1, cE1, cO1);
+    if (t1 < NT) compute(cE1, cO1);
     __syncwarp();
-    epilogue(tile, cE0, cO0);
+    epilogue(cE0, cO0);
     if (t1 >= NT) break;
     const int t2 = t1 + NW;
-    if (t2 < NT) compute(t2, cE0, cO0);
+    if (t2 < NT) compute(cE0, cO0);
     __syncwarp();
-    epilogue(t1, cE1, cO1);
+    epilogue(cE1, cO1);
     if (t2 >= NT) break;
     tile = t2;
   }
@@ -166,16 +180,20 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
     lo[ks] = kl * SO; hi[ks] = (m - 1 - kl) * SO;
     oo[ks] = (H + 1 + min(k, H - 1)) * SO;
   }
+  // columns n = p + MP q (x fastest) tracked incrementally: no per-tile div/mod (see eoc_lines)
+  constexpr int STEP = 8 * NW;
+  int nB = warp * 8 + g, qB = nB / MP, pB = nB - qB * MP;
+  int n0 = warp * 8 + 2 * t, q0 = n0 / MP, p0 = n0 - q0 * MP;
   for (int tile = warp; tile < NT; tile += NW) {
-    const int nb = min(tile * 8 + g, NCOL - 1);
-    const int qb = nb / MP, pb = nb - qb * MP;
-    double *xb = X + pb + qb * SQ;
+    double *xb = X + (nB < NCOL ? pB + qB * SQ : (MP - 1) + (MQ - 1) * SQ);
+    nB += STEP; pB += STEP % MP; qB += STEP / MP;
+    if (pB >= MP) { pB -= MP; ++qB; }
     double bE[KS], bO[KS], cE[MT][2], cO[MT][2];
     // eigen-divide factors of this lane's outputs, fetched before the DMMAs (L1/L2 table)
     double rE[MT][2], rO[MT][2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int n = min(tile * 8 + 2 * t + j, NCOL - 1);
+      const int n = min(n0 + j, NCOL - 1);
       const double *rc = Rz + (long long)n * m;        // column n = p + MP q, p = x fastest
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -202,11 +220,10 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
     int wb[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int n = tile * 8 + 2 * t + j;
       wb[j] = -1;
-      if (n >= NCOL) continue;
-      const int q = n / MP, p = n - q * MP;
-      wb[j] = p + q * SQ;
+      if (n0 + j >= NCOL) continue;
+      const bool carry = j && p0 + 1 >= MP;          // column n0 + 1 wraps to the next y row
+      wb[j] = carry ? (q0 + 1) * SQ : p0 + j + q0 * SQ;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int o = mt * 8 + g;
@@ -244,6 +261,8 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
         }
       }
     }
+    n0 += STEP; p0 += STEP % MP; q0 += STEP / MP;
+    if (p0 >= MP) { p0 -= MP; ++q0; }
   }
 }
 
