@@ -127,7 +127,8 @@ __device__ __forceinline__ void eo17_afrag(const double *__restrict__ Daug, doub
 
 template <int DIR, bool FIRST>
 __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
-                                           const double *af, const unsigned short *cmap) {
+                                           const double *af, const unsigned short *cmap,
+                                           const unsigned short *cmapY) {
   constexpr int n = 17, n2 = n * n, H = 8;
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
   constexpr int SO = DIR == 0 ? 1 : (DIR == 1 ? n : n2);
@@ -137,6 +138,12 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   if (warp >= NT) return;
+  // column nn = p + n q -> offset p SP + q SQ without a division: n nn (x pass), the cmapY
+  // table p + n^2 q (y pass), nn itself (z pass); the face coefficients sit at Cfd + nn
+  auto coloff = [&](int slot, int nn) {
+    (void)slot;
+    return DIR == 0 ? n * nn : (DIR == 1 ? (int)cmapY[slot] : nn);
+  };
   // A fragments (row i = g for E and O; tail row 8 for E), K slot k = 4 ks + t
   double aE[3], aO[3], at[3];
 #pragma unroll
@@ -157,16 +164,11 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     else { const int kk = k < H ? k : H; o1[ks] = kk * SO; o2[ks] = (n - 1 - kk) * SO; }
   }
   // one tile: B loads, 3 + 3 DMMAs (two accumulator chains), FMA tail row with a 2-step shuffle
-  auto compute = [&](int tile, double (&cE)[2], double (&cO)[2], double &tl, int &pb, int &qb) {
-#ifndef PMG_APPLY_NOCMAP
+  auto compute = [&](int tile, double (&cE)[2], double (&cO)[2], double &tl, int &ob) {
     const int nb = cmap[tile * 8 + g];
-#else
-    const int nb = min(tile * 8 + g, NCOL - 1);
-#endif
-    qb = nb / n;
-    pb = nb - qb * n;
-    const double *xb = U + pb * SP + qb * SQ;
-    const double *cb = Cfd + pb + n * qb;
+    ob = coloff(tile * 8 + g, nb);
+    const double *xb = U + ob;
+    const double *cb = Cfd + nb;
     double bE[3], bO[3];
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) {
@@ -187,43 +189,37 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     tl += __shfl_xor_sync(0xffffffffu, tl, 1);
     tl += __shfl_xor_sync(0xffffffffu, tl, 2);
   };
-  auto epilogue = [&](int tile, const double (&cE)[2], const double (&cO)[2], double tl, int pb, int qb) {
+  auto epilogue = [&](int tile, const double (&cE)[2], const double (&cO)[2], double tl, int ob) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int slot = tile * 8 + 2 * t + j;
       if (slot >= NCOL) continue;
-#ifndef PMG_APPLY_NOCMAP
-      const int nn = cmap[slot];
-#else
-      const int nn = slot;
-#endif
-      const int q = nn / n, p = nn - q * n;
-      double *vb = V + p * SP + q * SQ;
+      double *vb = V + coloff(slot, cmap[slot]);
       const double lo = cE[j] + cO[j], hi = cE[j] - cO[j];
       if (FIRST) { vb[g * SO] = lo; vb[(n - 1 - g) * SO] = hi; }
       else { vb[g * SO] += lo; vb[(n - 1 - g) * SO] += hi; }
     }
     if (t == 0 && tile * 8 + g < NCOL) {
-      double *vb = V + pb * SP + qb * SQ + H * SO;
+      double *vb = V + ob + H * SO;
       if (FIRST) *vb = tl;
       else *vb += tl;
     }
   };
   // software pipelined: the DMMAs of tile i + nw are issued before the epilogue of tile i
   double cE0[2], cO0[2], cE1[2], cO1[2], tl0, tl1;
-  int pb0, qb0, pb1, qb1;
+  int ob0, ob1;
   int tile = warp;
-  compute(tile, cE0, cO0, tl0, pb0, qb0);
+  compute(tile, cE0, cO0, tl0, ob0);
   for (;;) {
     const int t1 = tile + nw;
-    if (t1 < NT) compute(t1, cE1, cO1, tl1, pb1, qb1);
+    if (t1 < NT) compute(t1, cE1, cO1, tl1, ob1);
     __syncwarp();
-    epilogue(tile, cE0, cO0, tl0, pb0, qb0);
+    epilogue(tile, cE0, cO0, tl0, ob0);
     if (t1 >= NT) break;
     const int t2 = t1 + nw;
-    if (t2 < NT) compute(t2, cE0, cO0, tl0, pb0, qb0);
+    if (t2 < NT) compute(t2, cE0, cO0, tl0, ob0);
     __syncwarp();
-    epilogue(t1, cE1, cO1, tl1, pb1, qb1);
+    epilogue(t1, cE1, cO1, tl1, ob1);
     if (t2 >= NT) break;
     tile = t2;
   }
@@ -249,7 +245,8 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   double *Us = sm, *V = sm + n3 + 2, *Cf = V + n3, *ms = Cf + 12 * n2;
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(ms + 3 * n);
   unsigned short *cmap = reinterpret_cast<unsigned short *>(mbar + 1);      // n = 17 only
-  double *af17 = reinterpret_cast<double *>(cmap + ((PMG_COLMAP17_LEN + 3) & ~3));  // n = 17: 3 x EO17_AF
+  unsigned short *cmapY = cmap + ((PMG_COLMAP17_LEN + 3) & ~3);            // n = 17: p + n^2 q
+  double *af17 = reinterpret_cast<double *>(cmapY + ((PMG_COLMAP17_LEN + 3) & ~3));  // n = 17: 3 x EO17_AF
   const int edim[3] = {L.nx, L.ny, L.nz};
   const unsigned tbytes = 16u * n2;                                // 2 n^2 doubles per segment
   // Persistent: CTA b handles elements b, b + grid, ...  While element e is computed, the next
@@ -270,7 +267,11 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
   if (threadIdx.x == 0) mbar_init(mbar, 1);
   for (int d = 0; d < 3; ++d) stage(ms + d * n, L.mass[d], n);
   if constexpr (NT == 17) {
-    for (int i = threadIdx.x; i < PMG_COLMAP17_LEN; i += blockDim.x) cmap[i] = kColMap17[i];
+    for (int i = threadIdx.x; i < PMG_COLMAP17_LEN; i += blockDim.x) {
+      const int nn = kColMap17[i];
+      cmap[i] = (unsigned short)nn;
+      cmapY[i] = (unsigned short)(nn % n + n2 * (nn / n));
+    }
     const int w = threadIdx.x >> 5;
     if (w < 3) eo17_afrag(L.Daug[w], af17 + w * EO17_AF);
   }
@@ -341,10 +342,10 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
 #ifndef PMG_NO_APPLY_EO
     if constexpr (NT == 17) {            // even/odd passes (the transform stored -c4)
       PMG_APH(1);
-      apply_eo17<0, true>(U, Cf, V, af17, cmap); __syncthreads();
+      apply_eo17<0, true>(U, Cf, V, af17, cmap, cmapY); __syncthreads();
       PMG_APH(2);
-      apply_eo17<1, false>(U, Cf + 4 * n2, V, af17 + EO17_AF, cmap); __syncthreads();
-      apply_eo17<2, false>(U, Cf + 8 * n2, V, af17 + 2 * EO17_AF, cmap); __syncthreads();
+      apply_eo17<1, false>(U, Cf + 4 * n2, V, af17 + EO17_AF, cmap, cmapY); __syncthreads();
+      apply_eo17<2, false>(U, Cf + 8 * n2, V, af17 + 2 * EO17_AF, cmap, cmapY); __syncthreads();
       PMG_APH(3);
     } else
 #endif
@@ -506,7 +507,7 @@ bool apply_pipe_ok(const LevelDev &L) {
 
 static size_t apply_mma_smem(int n) {
   const size_t n2 = (size_t)n * n, n3 = n2 * n;
-  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2) + 2 * ((PMG_COLMAP17_LEN + 3) & ~3) +
+  return sizeof(double) * (2 * n3 + 2 + 12 * n2 + 3 * n + 2) + 4 * ((PMG_COLMAP17_LEN + 3) & ~3) +
          (n == 17 ? sizeof(double) * 3 * EO17_AF : 0);
 }
 
