@@ -318,11 +318,16 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
   {   // gather: flat over the window (all 32 lanes of every cp.async busy: LDGSTS issue, not
       // latency, bounds this phase — a row per warp left 32 - M0 lanes idle), padded plane stride
     const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
+#ifndef PMG_EXP_NOGATHER      // diagnostic: timing without the window gather (wrong results)
     for (int w = threadIdx.x; w < Mw; w += SH::THREADS) {
       const int bc = w / M0, a = w - bc * M0;
       const int c = bc / M1, b = bc - c * M1;
       cp_async8(X + a + M0 * b + S2 * c, r + xo[a] + yo[b] + zo[c]);
     }
+#else
+    (void)xo; (void)yo; (void)zo;
+    for (int w = threadIdx.x; w < S2 * M2; w += SH::THREADS) X[w] = 1.0;
+#endif
   }
 #endif
   cp_async_wait_all();
@@ -352,8 +357,13 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
     eoc_lines<0, SH, false, true>(X, Ss[0], wr);
   } else {
     const Blk G = {{M0, M1, M2}, {1, M0, M0 * M1}};   // global window order (Z)
+#ifndef PMG_EXP_NOSTORE       // diagnostic: last pass stores in place (no global Z store)
     EpiWeightStore ws{Z + (long long)e * Mw, G, {W[0], W[1], W[2]}};
     eoc_lines<0, SH, false, true>(X, Ss[0], ws);
+#else
+    eoc_lines<0, SH, false, true>(X, Ss[0], st);
+    if (threadIdx.x == 0) Z[(long long)e * Mw] = X[0];
+#endif
   }
 #ifdef PMG_PHASE_TIMING
   __syncthreads();
