@@ -26,7 +26,11 @@ template <int M0, int M1, int M2, bool WIDE = false, int TH = 0>
 struct Shape {
   static constexpr int S2 = plane_stride(M0, M1);
   static constexpr int Hmax = (M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2)) / 2;
+#ifdef PMG_EOC_THREADS23      // diagnostic: CTA width of the 23^3 kernel (e.g. 352 = 11 warps, 66 tiles / 11)
+  static constexpr int THREADS = TH ? TH : ((M0 == 23 && M1 == 23 && M2 == 23) ? PMG_EOC_THREADS23 : ((Hmax >= 8 || WIDE) ? 256 : 128));
+#else
   static constexpr int THREADS = TH ? TH : ((Hmax >= 8 || WIDE) ? 256 : 128);
+#endif
   static constexpr int MINB = Hmax >= 8 ? 2 : (WIDE ? 4 : 8);
   static constexpr int NWS = THREADS / 32;                    // warps per subdomain
   __device__ static __forceinline__ int wid() { return (int)(threadIdx.x >> 5); }
@@ -84,10 +88,20 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
     else { c.p += STEP % MP; c.q += STEP / MP; if (c.p >= MP) { c.p -= MP; ++c.q; } }
   };
   auto col_ok = [](const Col &c) { return QF ? c.p < MP : c.q < MQ; };
+  // Tile-column permutation pi = [0 1 2 3 5 4 7 6]: lane g loads column pi(g), C column index c
+  // is window column pi(c).  Consecutive columns are 4 double-banks apart (plane stride 4 mod 16,
+  // z fastest), so the B loads need pi(g) mod 4 distinct over each half-warp's four g and the C
+  // stores need pi(2t + j) mod 4 distinct over t: the identity order made the stores of lanes
+  // (g, t) and (g, t + 2) collide (ncu: 31 % of the kernel's shared-memory wavefronts).
+#ifdef PMG_EOC_PERM            // measured neutral (fdm@l4 1.229 vs 1.226 ms): the stores are not the limiter
+  auto pi = [](int c) { return c ^ ((c >> 2) & 1); };
+#else
+  auto pi = [](int c) { return c; };
+#endif
   Col cb, c0, c1;
-  col_init(warp * 8 + g, cb);
-  col_init(warp * 8 + 2 * t, c0);
-  col_init(warp * 8 + 2 * t + 1, c1);
+  col_init(warp * 8 + pi(g), cb);
+  col_init(warp * 8 + pi(2 * t), c0);
+  col_init(warp * 8 + pi(2 * t + 1), c1);
   auto compute = [&](double (&cE)[MT][2], double (&cO)[MT][2]) {
     const double *xb = X + (col_ok(cb) ? cb.p * SP + cb.q * SQ : (MP - 1) * SP + (MQ - 1) * SQ);
     col_adv(cb);
@@ -133,6 +147,47 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
     col_adv(c1);
   };
   double cE0[MT][2], cO0[MT][2], cE1[MT][2], cO1[MT][2];
+#ifdef PMG_EOC_PAIRED
+  // two tiles per step in one instruction stream (8 accumulator chains), no cross-step pipelining
+  auto loadB = [&](double (&bE)[KS], double (&bO)[KS]) {
+    const double *xb = X + (col_ok(cb) ? cb.p * SP + cb.q * SQ : (MP - 1) * SP + (MQ - 1) * SQ);
+    col_adv(cb);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double v1 = xb[off1[ks]], v2 = xb[off2[ks]];
+      if (FWD) { bE[ks] = v1 + v2; bO[ks] = v1 - v2; }
+      else { bE[ks] = v1; bO[ks] = v2; }
+    }
+  };
+  for (int tile = warp; tile < NT; tile += 2 * NW) {
+    if (tile + NW < NT) {
+      double bE0[KS], bO0[KS], bE1[KS], bO1[KS];
+      loadB(bE0, bO0);
+      loadB(bE1, bO1);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        cE0[mt][0] = cE0[mt][1] = cO0[mt][0] = cO0[mt][1] = 0.0;
+        cE1[mt][0] = cE1[mt][1] = cO1[mt][0] = cO1[mt][1] = 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          dmma884(cE0[mt][0], cE0[mt][1], aE[mt][ks], bE0[ks]);
+          dmma884(cO0[mt][0], cO0[mt][1], aO[mt][ks], bO0[ks]);
+          dmma884(cE1[mt][0], cE1[mt][1], aE[mt][ks], bE1[ks]);
+          dmma884(cO1[mt][0], cO1[mt][1], aO[mt][ks], bO1[ks]);
+        }
+      __syncwarp();
+      epilogue(cE0, cO0);
+      epilogue(cE1, cO1);
+    } else {
+      compute(cE0, cO0);
+      __syncwarp();
+      epilogue(cE0, cO0);
+    }
+  }
+#else
   int tile = warp;
   compute(cE0, cO0);
   for (;;) {
@@ -148,6 +203,7 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
     if (t2 >= NT) break;
     tile = t2;
   }
+#endif
 }
 
 // z passes fused: forward S_z^T, eigen-divide, backward S_z on warp-private z columns
@@ -182,7 +238,15 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
   }
   // columns n = p + MP q (x fastest) tracked incrementally: no per-tile div/mod (see eoc_lines)
   constexpr int STEP = 8 * NW;
+  // same tile-column permutation as eoc_lines: B column pi(g); for t >= 2 the lane's C columns
+  // 2t, 2t + 1 swap roles (sw)
+#ifdef PMG_EOC_PERM
+  const int sw = t >> 1;
+  int nB = warp * 8 + (g ^ ((g >> 2) & 1)), qB = nB / MP, pB = nB - qB * MP;
+#else
+  const int sw = 0;
   int nB = warp * 8 + g, qB = nB / MP, pB = nB - qB * MP;
+#endif
   int n0 = warp * 8 + 2 * t, q0 = n0 / MP, p0 = n0 - q0 * MP;
   for (int tile = warp; tile < NT; tile += NW) {
     double *xb = X + (nB < NCOL ? pB + qB * SQ : (MP - 1) + (MQ - 1) * SQ);
@@ -193,7 +257,7 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
     double rE[MT][2], rO[MT][2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const int n = min(n0 + j, NCOL - 1);
+      const int n = min(n0 + (j ^ sw), NCOL - 1);
       const double *rc = Rz + (long long)n * m;        // column n = p + MP q, p = x fastest
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -221,9 +285,10 @@ __device__ __forceinline__ void eoc_z_fused(double *X, const double *S, const do
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       wb[j] = -1;
-      if (n0 + j >= NCOL) continue;
-      const bool carry = j && p0 + 1 >= MP;          // column n0 + 1 wraps to the next y row
-      wb[j] = carry ? (q0 + 1) * SQ : p0 + j + q0 * SQ;
+      const int jj = j ^ sw;
+      if (n0 + jj >= NCOL) continue;
+      const bool carry = jj && p0 + 1 >= MP;         // column n0 + 1 wraps to the next y row
+      wb[j] = carry ? (q0 + 1) * SQ : p0 + jj + q0 * SQ;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int o = mt * 8 + g;
