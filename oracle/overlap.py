@@ -17,10 +17,14 @@ Readings (R5-R7):
 * Hat weight (Fig. 2 caption): xi_H = xi in the own element,
   xi -/+ 2 in the left/right neighbour; h = min(delta_ref, 1) (0 if the side has
   no overlap layer); t = (1 + h - |xi_H|) / (2 h) clipped to [0, 1];
-  w = q(t) = 10 t^3 - 15 t^4 + 6 t^5.  The quintic itself is the documented
-  choice (the exact one is in the absent [Stiller2016]): PARITY UNPINNED beyond
-  its stated shape (0 at the subdomain boundary, 1 on the non-overlapped core,
-  piecewise quintic) and partition of unity, which tests/ check.
+  w = q(t) = 10 t^3 - 15 t^4 + 6 t^5: the caption fixes "piece-wise quintic"; this is the
+  unique quintic with q(0) = 0, q(1) = 1 and C^2 contact at both ends (pinned by solving those
+  six conditions, tests/test_oracle_schwarz.py), and Table 1 discriminates it from the
+  lower-order transitions (cubic smoothstep: rows 9/13 come out 0.87/1.59 against the printed
+  1.15/1.75; linear ramp: 1.06 against 1.75; the quintic: 1.147/1.752 —
+  tests/test_oracle_mg.py::test_table1_rates_pin_the_quintic_transition).  What stays a reading
+  (the exact definition is in the absent [Stiller2016]) is the C^2 contact itself: a C^3 septic
+  smoothstep gives the same rates to 0.05, but is not "quintic".
 """
 import numpy as np
 from .basis import GLL, GL, face_distances

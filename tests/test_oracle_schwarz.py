@@ -126,3 +126,25 @@ def test_smoother_fixed_point():
     u = np.random.default_rng(2).uniform(-1, 1, d.N)
     f = d.apply(u)
     assert np.max(np.abs(d.smooth(u, f, 2) - u)) < 1e-12
+
+
+def test_quintic_is_the_c2_smoothstep():
+    """Fig. 2 caption: "piece-wise quintic transition from 0 ... to 1".  A quintic
+    has six coefficients; q(0) = 0, q(1) = 1 and vanishing first and second derivatives at both
+    ends (C^2 contact with the constant pieces) determine it uniquely.  Solve those six conditions
+    and compare with the oracle's transition on a grid (a dropped term or a wrong coefficient in
+    oracle.overlap.quintic fails this)."""
+    def row(t, der):
+        # d^der/dt^der of (1, t, ..., t^5) at t
+        r = np.zeros(6)
+        for k in range(der, 6):
+            c = 1.0
+            for j in range(der):
+                c *= (k - j)
+            r[k] = c * t ** (k - der)
+        return r
+    A = np.array([row(0, 0), row(0, 1), row(0, 2), row(1, 0), row(1, 1), row(1, 2)])
+    coef = np.linalg.solve(A, np.array([0, 0, 0, 1, 0, 0], dtype=float))
+    t = np.linspace(-0.25, 1.25, 61)
+    want = np.polynomial.polynomial.polyval(np.clip(t, 0, 1), coef)
+    assert np.max(np.abs(quintic(t) - want)) < 1e-14
