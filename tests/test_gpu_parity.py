@@ -252,6 +252,20 @@ BIG = [
 ]
 
 
+def test_very_large_windows_scalar_path():
+    """Windows beyond the global line-GEMM path (m > 80: P = 32 with n_o = 25 layers, m = 83) run the
+    scalar FP64 kernel k_fdm; one top-level Schwarz step against the oracle."""
+    c = Config("e-p32-no25", (4, 3, 3), (1.0, 1.0, 1.0), 32, 0, OverlapSpec(0, 25, 0))
+    g = _gpu(c)
+    assert g.level_overlap(g.L)[1] == [83, 83, 83]
+    H = MFHierarchy(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    f = uniform_zero_mean(c.ndofs, 0)
+    u = uniform_vector(c.ndofs, 1)
+    ug = _t(u)
+    g.schwarz_smooth(ug, _t(f), steps=1)
+    assert _rel(_n(ug), H.smooth(H.L, u, f, 1)) <= TOL
+
+
 @pytest.mark.parametrize("c", BIG, ids=[e.name for e in BIG])
 def test_large_windows_global_path(c):
     g = _gpu(c)
