@@ -333,7 +333,7 @@ int coarse_impl(dg_ctx *c, const double *f0, double *u0, cudaStream_t s) {
   }
   if (c->G[2] <= 32) {
     LAUNCHK(c, K_COARSE, 0, s, pmg::launch_coarse_fused(d0, C, f0, G1, G2, u0, s));
-    c->launches += 4;   // launch_coarse_fused issues 5 kernels
+    c->launches += pmg::coarse_fused_launches(C) - 1;   // launch_coarse_fused issues 3 or 5 kernels
     return PMG_OK;
   }
   LAUNCHK(c, K_COARSE, 0, s, pmg::launch_sum(f0, N0, part, scal + 10, 1.0 / N0, s));           // mean(f0)

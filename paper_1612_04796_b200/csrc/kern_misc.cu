@@ -580,6 +580,103 @@ __global__ void __launch_bounds__(512) k_coarse_cluster(CoarseDev C, int nx, int
   }
 }
 
+// Plane kernels for coarse grids beyond the cluster's reach (32^3: c3, c5): three launches instead
+// of five, every table read from shared memory without bank conflicts.
+//   k_coarse_plane_fwd  CTA = one z-plane, thread = (X', Y): stage the plane of f_0 (element-major
+//                       gather), x forward then y forward in shared memory -> G (lexicographic);
+//   k_coarse_zcols      CTA = 32 z columns, warp = one column, lane = z index: forward S_z^T,
+//                       eigen-divide (null mode -> 0), backward S_z with S_z and its transpose in
+//                       shared memory (the global-table version read rows with a 32-line stride);
+//   k_coarse_plane_bwd  CTA = one z-plane: y backward, x backward (transposed tables) -> u_0.
+__global__ void __launch_bounds__(1024) k_coarse_plane_fwd(CoarseDev C, int nx, int ny,
+                                                          const double *__restrict__ f0,
+                                                          double *__restrict__ G) {
+  extern __shared__ double sm[];
+  const int Gx = C.G[0], Gy = C.G[1], plane = Gx * Gy, Z = blockIdx.x;
+  double *A = sm, *B = A + plane, *Sx = B + plane, *Sy = Sx + Gx * Gx;
+  for (int i = threadIdx.x; i < Gx * Gx; i += blockDim.x) Sx[i] = C.S[0][i];
+  for (int i = threadIdx.x; i < Gy * Gy; i += blockDim.x) Sy[i] = C.S[1][i];
+  for (int g = threadIdx.x; g < plane; g += blockDim.x)
+    A[g] = __ldg(f0 + coarse_elem_index(nx, ny, g % Gx, g / Gx, Z));
+  __syncthreads();
+  for (int g = threadIdx.x; g < plane; g += blockDim.x) {
+    const int o = g % Gx;
+    const double *row = A + (g - o);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += Sx[k * Gx + o] * row[k];
+    B[g] = acc;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < plane; g += blockDim.x) {
+    const int a = g % Gx, o = g / Gx;
+    double acc = 0;
+    for (int k = 0; k < Gy; ++k) acc += Sy[k * Gy + o] * B[a + k * Gx];
+    G[g + (long long)plane * Z] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_coarse_zcols(CoarseDev C, double *__restrict__ G) {
+  extern __shared__ double sm[];
+  const int Gx = C.G[0], Gy = C.G[1], Gz = C.G[2];
+  const int cols = Gx * Gy;
+  double *Sz = sm, *SzT = Sz + Gz * Gz, *lz = SzT + Gz * Gz;
+  for (int i = threadIdx.x; i < Gz * Gz; i += blockDim.x) {
+    const double v = C.S[2][i];
+    Sz[i] = v;
+    SzT[(i % Gz) * Gz + i / Gz] = v;
+  }
+  for (int i = threadIdx.x; i < Gz; i += blockDim.x) lz[i] = C.lam[2][i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool zl = lane < Gz;
+  // issue the column loads before waiting for the tables
+  const int c0 = blockIdx.x * nw + warp;
+  const double v0 = (zl && c0 < cols) ? G[c0 + (long long)lane * cols] : 0.0;
+  __syncthreads();
+  for (int cidx = c0; cidx < cols; cidx += gridDim.x * nw) {
+    const int a = cidx % Gx, b = cidx / Gx;
+    const double v = cidx == c0 ? v0 : (zl ? G[cidx + (long long)lane * cols] : 0.0);
+    double acc = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double vk = __shfl_sync(0xffffffffu, v, k);
+      if (zl) acc += Sz[k * Gz + lane] * vk;
+    }
+    double w = 0.0;
+    if (zl && !(a == 0 && b == 0 && lane == 0)) w = acc / (C.lam[0][a] + C.lam[1][b] + lz[lane]);
+    double out = 0.0;
+    for (int k = 0; k < Gz; ++k) {
+      const double wk = __shfl_sync(0xffffffffu, w, k);
+      if (zl) out += SzT[k * Gz + lane] * wk;
+    }
+    if (zl) G[cidx + (long long)lane * cols] = out;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_coarse_plane_bwd(CoarseDev C, int nx, int ny,
+                                                          const double *__restrict__ G,
+                                                          double *__restrict__ u0) {
+  extern __shared__ double sm[];
+  const int Gx = C.G[0], Gy = C.G[1], plane = Gx * Gy, Z = blockIdx.x;
+  double *A = sm, *B = A + plane, *SxT = B + plane, *Sy = SxT + Gx * Gx;
+  for (int i = threadIdx.x; i < Gx * Gx; i += blockDim.x) SxT[(i % Gx) * Gx + i / Gx] = C.S[0][i];
+  for (int i = threadIdx.x; i < Gy * Gy; i += blockDim.x) Sy[i] = C.S[1][i];
+  for (int g = threadIdx.x; g < plane; g += blockDim.x) A[g] = G[g + (long long)plane * Z];
+  __syncthreads();
+  for (int g = threadIdx.x; g < plane; g += blockDim.x) {           // y backward (Y uniform per warp row)
+    const int a = g % Gx, Y = g / Gx;
+    double acc = 0;
+    for (int k = 0; k < Gy; ++k) acc += Sy[Y * Gy + k] * A[a + k * Gx];
+    B[g] = acc;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < plane; g += blockDim.x) {           // x backward -> element-major u_0
+    const int X = g % Gx, Y = g / Gx;
+    const double *row = B + (g - X);
+    double acc = 0;
+    for (int k = 0; k < Gx; ++k) acc += SxT[k * Gx + X] * row[k];
+    u0[coarse_elem_index(nx, ny, X, Y, Z)] = acc;
+  }
+}
+
 // x-backward pass writing u_0 in element-major order
 __global__ void k_coarse_xb(CoarseDev C, int nx, int ny, const double *__restrict__ G,
                             double *__restrict__ u0) {
@@ -885,13 +982,40 @@ cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const do
                                 double *G1, double *G2, double *u0, cudaStream_t s) {
   const long long N = (long long)C.G[0] * C.G[1] * C.G[2];
   const long long cols = (long long)C.G[0] * C.G[1];
+  if (C.G[2] > 32) return cudaErrorInvalidValue;
+#ifndef PMG_COARSE5
+  if (C.G[0] <= 32 && C.G[1] <= 32) {      // three plane / column launches (G1 only)
+    const int plane = C.G[0] * C.G[1];
+    const int th = std::min(1024, ((plane + 31) / 32) * 32);
+    const size_t sp = sizeof(double) * (2 * (size_t)plane + C.G[0] * C.G[0] + C.G[1] * C.G[1]);
+    const size_t sz = sizeof(double) * (2 * (size_t)C.G[2] * C.G[2] + C.G[2]);
+    static bool cfg = false;
+    if (!cfg) {
+      cfg = true;
+      cudaFuncSetAttribute(k_coarse_plane_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_coarse_plane_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_coarse_zcols, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    }
+    k_coarse_plane_fwd<<<C.G[2], th, sp, s>>>(C, L0.nx, L0.ny, f0, G1);
+    k_coarse_zcols<<<(int)((cols + 31) / 32), 1024, sz, s>>>(C, G1);
+    k_coarse_plane_bwd<<<C.G[2], th, sp, s>>>(C, L0.nx, L0.ny, G1, u0);
+    return cudaGetLastError();
+  }
+#endif
   k_coarse_xf<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, f0, G1);
   k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 1, G1, G2);
-  if (C.G[2] > 32) return cudaErrorInvalidValue;
   k_coarse_z<<<grid_for(cols * 32, 256), 256, 0, s>>>(C, G2);
   k_lex_contract<<<grid_for(N, 256), 256, 0, s>>>(C, 1, 0, G2, G1);
   k_coarse_xb<<<grid_for(N, 256), 256, 0, s>>>(C, L0.nx, L0.ny, G1, u0);
   return cudaGetLastError();
+}
+
+// kernels launched by launch_coarse_fused (for the launch counter)
+int coarse_fused_launches(const CoarseDev &C) {
+#ifndef PMG_COARSE5
+  if (C.G[0] <= 32 && C.G[1] <= 32) return 3;
+#endif
+  return 5;
 }
 
 cudaError_t launch_coarse_divide(const CoarseDev &C, double *G, cudaStream_t s) {

@@ -90,6 +90,7 @@ cudaError_t launch_coarse_fused(const LevelDev &L0, const CoarseDev &C, const do
 bool coarse_one_ok(const CoarseDev &C);
 // one 8-CTA cluster, z pass through distributed shared memory (1024 < N_0, every G_d <= 32)
 bool coarse_cluster_ok(const CoarseDev &C);
+int coarse_fused_launches(const CoarseDev &C);
 cudaError_t launch_coarse_cluster(const LevelDev &L0, const CoarseDev &C, const double *f0, double *u0,
                                   cudaStream_t s);
 cudaError_t launch_coarse_one(const LevelDev &L0, const CoarseDev &C, const double *f0, double *u0,

@@ -402,11 +402,12 @@ def test_vector_helpers_and_coarse_at_c3_size():
 
 
 @pytest.mark.parametrize("ne,length", [((6, 5, 7), (1.0, 1.0, 1.0)), ((16, 4, 9), (3.0, 1.0, 2.0)),
-                                       ((5, 6, 16), (1.0, 2.0, 1.0)), ((8, 8, 8), (1.0, 1.0, 1.0))])
+                                       ((5, 6, 16), (1.0, 2.0, 1.0)), ((8, 8, 8), (1.0, 1.0, 1.0)),
+                                       ((16, 12, 14), (1.0, 1.0, 1.0)), ((9, 16, 11), (2.0, 1.0, 1.0))])
 def test_coarse_cluster_ragged(ne, length):
     """Coarse pseudo-inverse (Alg. 1 l.295) on the one-cluster path with non-cubic grids whose
     z extent does not divide evenly over the 8 CTAs (G_z = 14, 18, 32; some CTAs own no plane),
-    and on c2's 16^3 grid."""
+    and on c2's 16^3 grid; the last two grids (N_0 > 8192) take the three-launch plane path."""
     c = Config("coarse", ne, length, 2, 0, OverlapSpec(0, 1, 0))
     g = _gpu(c)
     H = _oracle(c)
