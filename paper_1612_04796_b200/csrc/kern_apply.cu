@@ -415,6 +415,123 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
 #undef PMG_APH
 }
 
+// Small elements (n = 3, 5: the two lowest smoothing levels of every configuration): EPB
+// elements per 256-thread CTA, one thread per DOF, plain FP64 FMAs (Eq. 7 / Eq. 8, PAPER.md:
+// 149-164, :192-200) and the fused residual restriction (Alg. 1 l.292) as three small passes in
+// shared memory.  A 27- or 125-DOF element cannot feed a CTA of DMMA line GEMMs: the persistent
+// k_apply_mma<3/5> spent ~5 us per element in ~10 block barriers (19-23 us per launch on c3's
+// 4096 elements, 9 us on one-wave meshes); here every load of a thread is independent and issued
+// up front, one barrier before the restriction passes.  Same operator tables (Daug rows
+// pre-scaled by 1/M_d, face couplings as four extra columns) as the DMMA path.
+template <int NT, int EPB>
+__global__ void __launch_bounds__(256) k_apply_small(LevelDev L, const double *__restrict__ u,
+                                                     const double *__restrict__ T,
+                                                     const double *__restrict__ f,
+                                                     double *__restrict__ out,
+                                                     const double *__restrict__ restrict_I,
+                                                     double *__restrict__ fc) {
+  constexpr int n = NT, n2 = n * n, n3 = n2 * n, KA = n + 4, NC = (NT + 1) / 2;
+  __shared__ double Us[EPB * n3];
+  __shared__ double Da[3 * n * KA];
+  __shared__ double ms[3 * n];
+  __shared__ double Ic[n * NC];
+  __shared__ double R1[EPB * NC * n2];
+  __shared__ double R2[EPB * NC * NC * n];
+  const int e0 = blockIdx.x * EPB;
+  const int ne = min(EPB, L.Ne - e0);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < ne * n3; i += blockDim.x) Us[i] = __ldg(u + (long long)e0 * n3 + i);
+  for (int i = tid; i < 3 * n * KA; i += blockDim.x) Da[i] = L.Daug[i / (n * KA)][i % (n * KA)];
+  for (int i = tid; i < 3 * n; i += blockDim.x) ms[i] = L.mass[i / n][i % n];
+  if (restrict_I)
+    for (int i = tid; i < n * NC; i += blockDim.x) Ic[i] = restrict_I[i];
+  const int le = tid / n3, t = tid - le * n3;
+  const bool act = le < ne;
+  const int e = e0 + (act ? le : 0);
+  const int i0 = t % n, j0 = (t / n) % n, k0 = t / n2;
+  // neighbour traces of the three lines through this DOF (L2 / L1 hits), issued before the barrier
+  double c[3][4];
+  {
+    const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
+    const int edim[3] = {L.nx, L.ny, L.nz};
+    const int pface[3] = {j0 + n * k0, i0 + n * k0, i0 + n * j0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      int cc[3] = {ec[0], ec[1], ec[2]};
+      cc[d] = wrap(ec[d] + 1, edim[d]);
+      const long long nbR = cc[0] + L.nx * (cc[1] + (long long)L.ny * cc[2]);
+      cc[d] = wrap(ec[d] - 1, edim[d]);
+      const long long nbL = cc[0] + L.nx * (cc[1] + (long long)L.ny * cc[2]);
+      const double *TR = T + (nbR * 3 + d) * 4 * n2 + pface[d];
+      const double *TL = T + (nbL * 3 + d) * 4 * n2 + pface[d];
+      const double tvR = act ? __ldg(TR) : 0.0, tdR = act ? __ldg(TR + n2) : 0.0;
+      const double tvL = act ? __ldg(TL + 2 * n2) : 0.0, tdL = act ? __ldg(TL + 3 * n2) : 0.0;
+      const double mu = L.mu[d];
+      c[d][0] = -0.5 * tdR - mu * tvR;
+      c[d][1] = 0.5 * tvR;
+      c[d][2] = 0.5 * tdL - mu * tvL;
+      c[d][3] = -0.5 * tvL;
+    }
+  }
+  const long long g = (long long)e * n3 + t;
+  const double fv = (act && f) ? __ldg(f + g) : 0.0;
+  __syncthreads();
+  double r = 0.0;
+  if (act) {
+    const int idx[3] = {i0, j0, k0};
+    const int stride[3] = {1, n, n2};
+    double v = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double *Dr = Da + d * n * KA + idx[d] * KA;
+      const double *line = Us + le * n3 + (t - idx[d] * stride[d]);
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < n; ++m) acc = fma(Dr[m], line[m * stride[d]], acc);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc = fma(Dr[n + q], c[d][q], acc);
+      v += acc;
+    }
+    const double mv = ms[i0] * ms[n + j0] * ms[2 * n + k0] * v;
+    r = f ? fv - mv : mv;
+    if (!restrict_I) out[g] = r;
+  }
+  if (!restrict_I) return;
+  // fused residual restriction f_c = (I^T (x) I^T (x) I^T) r: r replaces u in shared memory
+  __syncthreads();
+  if (act) Us[le * n3 + t] = r;
+  __syncthreads();
+  for (int w = tid; w < ne * NC * n2; w += blockDim.x) {          // x: n -> NC
+    const int lb = w / (NC * n2), q = w - lb * NC * n2;
+    const int o = q % NC, jk = q / NC;
+    const double *row = Us + lb * n3 + n * jk;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < n; ++m) acc = fma(Ic[m * NC + o], row[m], acc);
+    R1[w] = acc;
+  }
+  __syncthreads();
+  for (int w = tid; w < ne * NC * NC * n; w += blockDim.x) {      // y: n -> NC
+    const int lb = w / (NC * NC * n), q = w - lb * NC * NC * n;
+    const int o1 = q % NC, o2 = (q / NC) % NC, k = q / (NC * NC);
+    const double *col = R1 + lb * NC * n2 + o1 + NC * n * k;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < n; ++m) acc = fma(Ic[m * NC + o2], col[NC * m], acc);
+    R2[w] = acc;
+  }
+  __syncthreads();
+  for (int w = tid; w < ne * NC * NC * NC; w += blockDim.x) {     // z: n -> NC, to the coarse vector
+    const int lb = w / (NC * NC * NC), q = w - lb * NC * NC * NC;
+    const int o12 = q % (NC * NC), o3 = q / (NC * NC);
+    const double *col = R2 + lb * NC * NC * n + o12;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < n; ++m) acc = fma(Ic[m * NC + o3], col[NC * NC * m], acc);
+    fc[(long long)(e0 + lb) * NC * NC * NC + q] = acc;
+  }
+}
+
 // Face traces with the element staged in shared memory (coalesced loads).
 __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__restrict__ u,
                                                    double *__restrict__ T) {
@@ -528,6 +645,13 @@ static void launch_apply_nt(const LevelDev &L, const double *u, const double *T,
   // persistent grid: as many CTAs as fit on the device at once (occupancy x SMs), capped at Ne;
   // a mesh that fits in one wave of 4 CTAs per SM gets 256-thread CTAs (latency-bound regime)
   const size_t sb = apply_mma_smem(NT);
+#ifndef PMG_NO_APPLY_SMALL
+  if constexpr (NT == 3 || NT == 5) {       // several elements per CTA, thread per DOF
+    constexpr int EPB = NT == 3 ? 9 : 2;
+    k_apply_small<NT, EPB><<<(int)((L.Ne + EPB - 1) / EPB), 256, 0, s>>>(L, u, T, f, out, I, fc);
+    return;
+  }
+#endif
   if (NT <= 9 && L.Ne <= 4LL * num_sms()) {
     static bool cfg = false;
     if (!cfg) {
