@@ -90,6 +90,18 @@ int dg_residual(dg_ctx *ctx, int level, const double *u, const double *f, double
  * u is updated in place; f is read-only. */
 int schwarz_smooth(dg_ctx *ctx, int level, double *u, const double *f, int steps, void *stream);
 
+/* The two halves of one Schwarz step, for callers that must exchange data between them (element
+ * slabs on several GPUs): dg_schwarz_solve computes the weighted subdomain solutions
+ * W_s A_ss^{-1} R_s r of every subdomain of level l into the context's window buffer
+ * (PAPER.md:201-232); dg_schwarz_fold adds their deterministic sum (Eq. 10) to
+ * u (zero != 0: u is overwritten by the sum).  schwarz_smooth = dg_residual, dg_schwarz_solve,
+ * dg_schwarz_fold.  dg_window_buffer returns where the window buffer of level l lives inside the
+ * bound workspace (byte offset) and its doubles per subdomain; subdomain s = element s, stored
+ * contiguously in element order.  Errors: PMG_EINVAL, PMG_ESTATE. */
+int dg_schwarz_solve(dg_ctx *ctx, int level, const double *r, void *stream);
+int dg_schwarz_fold(dg_ctx *ctx, int level, double *u, int zero, void *stream);
+int dg_window_buffer(const dg_ctx *ctx, int level, size_t *byte_offset, long long *doubles_per_subdomain);
+
 /* Level transfers: prolongation uf += I_l uc (level l from l-1) and residual
  * restriction fc = I_l^T rf. */
 int dg_prolongate_add(dg_ctx *ctx, int level, const double *uc, double *uf, void *stream);
@@ -138,6 +150,10 @@ int pcg_solve(dg_ctx *ctx, double *u, const double *f, double rtol, int maxit, i
  * dg_dot -> *out_host = <x, y>  (synchronises);  dg_project_mean: v -= mean(v). */
 int dg_dot(dg_ctx *ctx, int level, const double *x, const double *y, double *out_host, void *stream);
 int dg_project_mean(dg_ctx *ctx, int level, double *v, void *stream);
+/* <x, y> over the first `count` entries (count <= top-level DOFs; synchronises): the owned part
+ * of a slab-decomposed vector. */
+int dg_dot_range(dg_ctx *ctx, const double *x, const double *y, long long count, double *out_host,
+                 void *stream);
 
 /* dg_rhs_sin — b = M * amp * sin(kx x) sin(ky y) sin(kz z) at the top-level nodes (diagonal
  * GL/GLL quadrature of the load term), then b -= mean(b). */

@@ -7,4 +7,6 @@ shared library is missing this import fails.
 from .binding import (DG, lib, PMGError, GLL, GL, OVL_NODES, OVL_REL, OVL_MAXREL,  # noqa: F401
                       dg_setup)
 
-__all__ = ["DG", "dg_setup", "PMGError", "GLL", "GL", "OVL_NODES", "OVL_REL", "OVL_MAXREL"]
+from .slab import SlabDG  # noqa: F401,E402
+
+__all__ = ["DG", "SlabDG", "dg_setup", "PMGError", "GLL", "GL", "OVL_NODES", "OVL_REL", "OVL_MAXREL"]

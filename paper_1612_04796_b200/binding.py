@@ -29,6 +29,10 @@ _sig = {
     "dg_apply": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dg_residual": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "schwarz_smooth": (_i, [_vp, _i, _vp, _vp, _i, _vp]),
+    "dg_schwarz_solve": (_i, [_vp, _i, _vp, _vp]),
+    "dg_schwarz_fold": (_i, [_vp, _i, _vp, _i, _vp]),
+    "dg_window_buffer": (_i, [_vp, _i, C.POINTER(_sz), C.POINTER(_ll)]),
+    "dg_dot_range": (_i, [_vp, _vp, _vp, _ll, _dp, _vp]),
     "dg_prolongate_add": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dg_restrict": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dg_coarse_solve": (_i, [_vp, _vp, _vp, _vp]),
@@ -182,6 +186,40 @@ class DG:
         n = self.ndofs(level)
         self._check(lib.schwarz_smooth(self._c, level, _vec(u, n, "u"), _vec(f, n, "f"), int(steps), _stream()))
         return u
+
+    def schwarz_solve(self, r, level=None):
+        """First half of a Schwarz step: weighted subdomain solutions of r into the window buffer."""
+        level = self.L if level is None else level
+        self._check(lib.dg_schwarz_solve(self._c, level, _vec(r, self.ndofs(level), "r"), _stream()))
+
+    def schwarz_fold(self, u, zero=False, level=None):
+        """Second half: u (+)= deterministic sum of the weighted subdomain solutions."""
+        level = self.L if level is None else level
+        self._check(lib.dg_schwarz_fold(self._c, level, _vec(u, self.ndofs(level), "u"), 1 if zero else 0,
+                                        _stream()))
+        return u
+
+    def window_buffer(self, level=None):
+        """Zero-copy float64 view of level l's window buffer inside the workspace
+        (subdomains in element order, dg_window_buffer doubles each)."""
+        import torch
+        level = self.L if level is None else level
+        off, per = _sz(0), _ll(0)
+        self._check(lib.dg_window_buffer(self._c, level, C.byref(off), C.byref(per)))
+        ne = self.ne[0] * self.ne[1] * self.ne[2]
+        nbytes = 8 * per.value * ne
+        return self.ws[off.value: off.value + nbytes].view(torch.float64), per.value
+
+    def dot_range(self, x, y, count):
+        """<x, y> over the first `count` entries of two contiguous CUDA float64 tensors."""
+        import torch
+        for t in (x, y):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                    and t.numel() >= count):
+                raise ValueError("dot_range: need contiguous CUDA float64 tensors with >= count entries")
+        v = C.c_double(0)
+        self._check(lib.dg_dot_range(self._c, _ptr(x), _ptr(y), int(count), C.byref(v), _stream()))
+        return v.value
 
     def prolongate_add(self, uc, uf, level):
         self._check(lib.dg_prolongate_add(self._c, level, _vec(uc, self.ndofs(level - 1), "uc"),

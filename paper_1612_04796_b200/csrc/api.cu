@@ -274,6 +274,25 @@ int residual_impl(dg_ctx *c, int l, const double *u, const double *f, double *ou
   return PMG_OK;
 }
 
+// All subdomain solves of level l: Z_l = W_s A_ss^{-1} R_s r for every element-centred subdomain
+// (window-major weighted results; the fold sums them).
+int fdm_impl(dg_ctx *c, int l, const double *rin, cudaStream_t s) {
+  LevelHost &h = c->lev[l];
+  pmg::LevelDev d = level_dev(c, l);
+  double *Z = wsp<double>(c, h.o_Z);
+  double *scr = h.o_scr ? wsp<double>(c, h.o_scr) : nullptr;
+  if (h.fdm_path == 1 && pmg::fdm45_ok(d)) {
+    LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm45(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
+    c->launches += 2;
+  } else if (h.fdm_path == 1) {
+    LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_global(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
+    c->launches += 6;
+  } else {
+    LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
+  }
+  return PMG_OK;
+}
+
 // `steps` Schwarz iterations.  traces_after: the last fold also emits the traces of the final u
 // (the caller's next operation is a residual of u on this level).
 int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool zero_init,
@@ -301,15 +320,8 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
       if (emit) LAUNCHK(c, K_TRACES, l, s, pmg::launch_traces(d, u, T, s));
       continue;
     }
-    if (h.fdm_path == 1 && pmg::fdm45_ok(d)) {
-      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm45(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
-      c->launches += 2;
-    } else if (h.fdm_path == 1) {
-      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm_global(d, rin, scr, wsp<double>(c, h.o_scr2), Z, s));
-      c->launches += 6;
-    } else {
-      LAUNCHK(c, K_FDM, l, s, pmg::launch_fdm(d, rin, Z, scr, h.fdm_smem, h.fdm_smem_bytes, s));
-    }
+    int st = fdm_impl(c, l, rin, s);
+    if (st) return st;
     LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, emit ? T : nullptr, s));
   }
   if (steps == 0 && zero_init) LAUNCH(c, pmg::launch_zero(u, h.N, s));
@@ -675,6 +687,51 @@ int schwarz_smooth(dg_ctx *c, int level, double *u, const double *f, int steps, 
   if (!c->schwarz_ready) return fail(c, PMG_ESTATE, "dg_schwarz_setup not called");
   if (!u || !f || steps < 0) return fail(c, PMG_EINVAL, "schwarz_smooth: bad arguments");
   return smooth_impl(c, level, u, f, steps, false, S(stream));
+}
+
+int dg_schwarz_solve(dg_ctx *c, int level, const double *r, void *stream) {
+  int st = check_level(c, level);
+  if (st) return st;
+  if (level < 1) return fail(c, PMG_EINVAL, "no smoother on the coarse level");
+  if (!c->schwarz_ready) return fail(c, PMG_ESTATE, "dg_schwarz_setup not called");
+  if (!r) return fail(c, PMG_EINVAL, "dg_schwarz_solve: null vector");
+  return fdm_impl(c, level, r, S(stream));
+}
+
+int dg_schwarz_fold(dg_ctx *c, int level, double *u, int zero, void *stream) {
+  int st = check_level(c, level);
+  if (st) return st;
+  if (level < 1) return fail(c, PMG_EINVAL, "no smoother on the coarse level");
+  if (!c->schwarz_ready) return fail(c, PMG_ESTATE, "dg_schwarz_setup not called");
+  if (!u) return fail(c, PMG_EINVAL, "dg_schwarz_fold: null vector");
+  pmg::LevelDev d = level_dev(c, level);
+  cudaStream_t s = S(stream);
+  LAUNCHK(c, K_FOLD, level, s, pmg::launch_fold(d, wsp<double>(c, c->lev[level].o_Z), u, zero != 0, nullptr, s));
+  return PMG_OK;
+}
+
+int dg_window_buffer(const dg_ctx *c, int level, size_t *byte_offset, long long *doubles_per_subdomain) {
+  if (!c || level < 1 || level > c->L || !c->schwarz_ready || !byte_offset || !doubles_per_subdomain)
+    return PMG_EINVAL;
+  *byte_offset = c->lev[level].o_Z;
+  *doubles_per_subdomain = c->lev[level].Mw;
+  return PMG_OK;
+}
+
+int dg_dot_range(dg_ctx *c, const double *x, const double *y, long long count, double *out_host,
+                 void *stream) {
+  if (!c) return PMG_EINVAL;
+  if (!c->ws) return fail(c, PMG_ESTATE, "workspace not bound");
+  if (!x || !y || !out_host || count < 0 || count > c->lev[c->L].N)
+    return fail(c, PMG_EINVAL, "dg_dot_range: bad arguments");
+  cudaStream_t s = S(stream);
+  double *part = wsp<double>(c, c->o_part), *scal = wsp<double>(c, c->o_scal);
+  LAUNCH(c, pmg::launch_dot(x, y, count, part, scal + 20, s));
+  cudaError_t e = cudaMemcpyAsync(c->host_pinned, scal + 20, sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_check(c, e, "dg_dot_range");
+  *out_host = c->host_pinned[0];
+  return PMG_OK;
 }
 
 int dg_prolongate_add(dg_ctx *c, int level, const double *uc, double *uf, void *stream) {
