@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/pmg_dg.h"
 #include "kernels.cuh"
 #include "setup.hpp"
@@ -231,13 +233,25 @@ cudaEvent_t prof_event(dg_ctx *c, size_t i) {
   return c->ev_pool[i];
 }
 
+// NVTX ranges "kind@level" around every launch (timeline tools), enabled by PMG_NVTX=1 in the
+// environment; header-only NVTX v3, a no-op without an attached tool.
+const bool g_nvtx = [] { const char *e = std::getenv("PMG_NVTX"); return e && e[0] == '1'; }();
+void nvtx_push(int kind, int level) {
+  static const char *names[8] = {"traces", "apply", "fdm", "fold", "restrict", "prolong", "coarse", "vec"};
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%s@l%d", names[kind & 7], level);
+  nvtxRangePushA(buf);
+}
+
 // Every kernel launch goes through here: counts launches and (if enabled) brackets the launch
 // with CUDA events on the launching stream.
 #define LAUNCHK(c, kind, level, s, expr)                                         \
   do {                                                                           \
     size_t _pi = (c)->ev_slot.size();                                            \
     if ((c)->prof) cudaEventRecord(prof_event((c), 2 * _pi), (s));               \
+    if (g_nvtx) nvtx_push((kind), (level));                                      \
     cudaError_t _e = (expr);                                                     \
+    if (g_nvtx) nvtxRangePop();                                                  \
     (c)->launches++;                                                             \
     if ((c)->prof) {                                                             \
       cudaEventRecord(prof_event((c), 2 * _pi + 1), (s));                        \
