@@ -154,6 +154,10 @@ int dg_project_mean(dg_ctx *ctx, int level, double *v, void *stream);
  * of a slab-decomposed vector. */
 int dg_dot_range(dg_ctx *ctx, const double *x, const double *y, long long count, double *out_host,
                  void *stream);
+/* y = a x + b y over `count` entries with host scalars (b == 0: y = a x, y is not read): the
+ * vector updates of a host-driven Krylov loop (slab-decomposed inexact PCG, PAPER.md:309-311,
+ * whose alpha and beta are all-reduced over the ranks first). */
+int dg_axpby(dg_ctx *ctx, double *y, double a, const double *x, double b, long long count, void *stream);
 
 /* dg_rhs_sin — b = M * amp * sin(kx x) sin(ky y) sin(kz z) at the top-level nodes (diagonal
  * GL/GLL quadrature of the load term), then b -= mean(b). */

@@ -33,6 +33,7 @@ _sig = {
     "dg_schwarz_fold": (_i, [_vp, _i, _vp, _i, _vp]),
     "dg_window_buffer": (_i, [_vp, _i, C.POINTER(_sz), C.POINTER(_ll)]),
     "dg_dot_range": (_i, [_vp, _vp, _vp, _ll, _dp, _vp]),
+    "dg_axpby": (_i, [_vp, _vp, _d, _vp, _d, _ll, _vp]),
     "dg_prolongate_add": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dg_restrict": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dg_coarse_solve": (_i, [_vp, _vp, _vp, _vp]),
@@ -220,6 +221,17 @@ class DG:
         v = C.c_double(0)
         self._check(lib.dg_dot_range(self._c, _ptr(x), _ptr(y), int(count), C.byref(v), _stream()))
         return v.value
+
+    def axpby(self, y, a, x, b=1.0):
+        """y = a x + b y (same-size contiguous CUDA float64 tensors)."""
+        import torch
+        for t in (x, y):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ValueError("axpby: need contiguous CUDA float64 tensors")
+        if x.numel() != y.numel():
+            raise ValueError("axpby: size mismatch")
+        self._check(lib.dg_axpby(self._c, _ptr(y), float(a), _ptr(x), float(b), y.numel(), _stream()))
+        return y
 
     def prolongate_add(self, uc, uf, level):
         self._check(lib.dg_prolongate_add(self._c, level, _vec(uc, self.ndofs(level - 1), "uc"),

@@ -748,6 +748,14 @@ int dg_dot_range(dg_ctx *c, const double *x, const double *y, long long count, d
   return PMG_OK;
 }
 
+int dg_axpby(dg_ctx *c, double *y, double a, const double *x, double b, long long count, void *stream) {
+  if (!c) return PMG_EINVAL;
+  if (!x || !y || count < 0) return fail(c, PMG_EINVAL, "dg_axpby: bad arguments");
+  cudaStream_t s = S(stream);
+  LAUNCH(c, pmg::launch_axpby(y, a, x, b, count, s));
+  return PMG_OK;
+}
+
 int dg_prolongate_add(dg_ctx *c, int level, const double *uc, double *uf, void *stream) {
   int st = check_level(c, level);
   if (st) return st;

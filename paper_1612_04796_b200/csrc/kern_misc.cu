@@ -760,6 +760,14 @@ __global__ void k_copy(double *__restrict__ d, const double *__restrict__ s, lon
     d[g] = s ? s[g] : 0.0;
 }
 
+// y = a x + b y with host scalars (b == 0: y = a x without reading y): the vector updates of a
+// Krylov loop driven from the host (slab-decomposed PCG, whose scalars are all-reduced first)
+__global__ void k_axpby(double *__restrict__ y, double a, const double *__restrict__ x, double b, long long N) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N;
+       g += (long long)gridDim.x * blockDim.x)
+    y[g] = b == 0.0 ? (a == 0.0 ? 0.0 : a * x[g]) : fma(a, x[g], b * y[g]);   // a = b = 0: y = 0 exactly
+}
+
 __global__ void k_cg_update(double *__restrict__ u, double *__restrict__ r, double *__restrict__ rold,
                             const double *__restrict__ p, const double *__restrict__ q, long long N,
                             double *__restrict__ part, const double *__restrict__ scal) {
@@ -1057,6 +1065,10 @@ cudaError_t launch_copy(double *dst, const double *src, long long N, cudaStream_
   return cudaGetLastError();
 }
 cudaError_t launch_zero(double *dst, long long N, cudaStream_t s) { return launch_copy(dst, nullptr, N, s); }
+cudaError_t launch_axpby(double *y, double a, const double *x, double b, long long N, cudaStream_t s) {
+  k_axpby<<<grid_for(N, 256), 256, 0, s>>>(y, a, x, b, N);
+  return cudaGetLastError();
+}
 cudaError_t launch_pq_alpha(const double *p, const double *q, long long N, double *partial,
                             double *scal, cudaStream_t s) {
   const int nb = reduce_blocks(N);

@@ -107,6 +107,7 @@ cudaError_t launch_dot(const double *x, const double *y, long long N, double *pa
 cudaError_t launch_sub_scalar(double *v, long long N, const double *c, cudaStream_t s);
 cudaError_t launch_copy(double *dst, const double *src, long long N, cudaStream_t s);
 cudaError_t launch_zero(double *dst, long long N, cudaStream_t s);
+cudaError_t launch_axpby(double *y, double a, const double *x, double b, long long N, cudaStream_t s);
 // PCG (Golub-Ye) helpers; scal[] slots documented in api.cu
 cudaError_t launch_pq_alpha(const double *p, const double *q, long long N, double *partial,
                             double *scal, cudaStream_t s);

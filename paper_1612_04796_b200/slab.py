@@ -18,8 +18,8 @@ be refreshed.  One weighted Schwarz step (Eq. 10) on level l i
 
 The transfers are element-local; the restricted right-hand side gets its ghosts exchanged; the
 coarse problem (8 DOF per element) is all-gathered and solved redundantly on every rank with the
-global coarse pseudo-inverse (Alg. 1 l.295); residual norms are all-reduced.  (The inexact PCG of
-config 5 is not decomposed yet: it needs the same exchanges plus all-reduced scalars.)  Arithmetic per owned
+global coarse pseudo-inverse (Alg. 1 l.295); residual norms and the scalars of the inexact PCG
+ are all-reduced, its vector updates run through dg_axpby.  Arithmetic per owned
 DOF is that of the single-GPU path (same kernels, same tables, same fold order).
 
 This module is orchestration only (which ABI call and which exchange, in which order); the
@@ -142,6 +142,11 @@ class SlabDG:
         self.exchange(u, self.n[level] ** 3)
         return self.g.residual(u, f, level=level, out=self._r[level] if out is None else out)
 
+    def apply(self, u, out, level=None):
+        level = self.L if level is None else level
+        self.exchange(u, self.n[level] ** 3)
+        return self.g.apply(u, level=level, out=out)
+
     def smooth(self, level, u, f, steps, zero):
         """`steps` weighted Schwarz iterations; zero: u == 0 on entry (r = f, Alg. 1 l.287-290;
         the ghosts of f must be valid)."""
@@ -211,3 +216,38 @@ class SlabDG:
             if not math.isfinite(hist[-1]) or hist[-1] > 1e3 * hist[0]:
                 return u, hist, False
         return u, hist, hist[-1] <= rtol * hist[0]
+
+    # ---- inexact PCG (Golub-Ye), PAPER.md:309-311 ---------------------------------------------
+    def pcg_solve(self, u, f, rtol=1e-10, maxit=100):
+        """MG-preconditioned inexact CG on slabs: the library's recurrence (z = one V-cycle from
+        zero, beta = <z, r - r_old> / <z_old, r_old>), dots all-reduced, vector updates through
+        dg_axpby on the local vectors (ghost entries are refreshed by the next exchange).
+        Returns (u, residual history, converged)."""
+        g, torch = self.g, self.torch
+        r = torch.empty_like(u)
+        self.residual(u, f, out=r)
+        hist = [math.sqrt(self.dot(r, r))]
+        if hist[0] == 0.0:
+            return u, hist, True
+        z, p, q, rold = (torch.zeros_like(u) for _ in range(4))
+        self.vcycle(z, r)
+        g.axpby(p, 1.0, z, 0.0)
+        zr_old = self.dot(z, r)
+        for _ in range(maxit):
+            self.apply(p, q)
+            alpha = zr_old / self.dot(p, q)
+            g.axpby(u, alpha, p, 1.0)
+            g.axpby(rold, 1.0, r, 0.0)
+            g.axpby(r, -alpha, q, 1.0)
+            hist.append(math.sqrt(self.dot(r, r)))
+            if not math.isfinite(hist[-1]) or hist[-1] > 1e3 * hist[0]:
+                return u, hist, False
+            if hist[-1] <= rtol * hist[0]:
+                return u, hist, True
+            g.axpby(z, 0.0, z, 0.0)                       # z = 0: V-cycle from a zero guess
+            self.vcycle(z, r)
+            zr = self.dot(z, r)
+            beta = (zr - self.dot(z, rold)) / zr_old
+            zr_old = zr
+            g.axpby(p, 1.0, z, beta)
+        return u, hist, False

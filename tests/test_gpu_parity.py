@@ -542,3 +542,24 @@ def test_slab_decomposition_single_rank_equals_plain(name, ne):
     r_plain = g.residual(u_plain, fg)
     r_slab = sd.residual(ul, fl)
     assert abs(sd.dot(r_slab, r_slab) - g.dot(r_plain, r_plain)) <= 1e-10 * g.dot(r_plain, r_plain)
+
+
+@pytest.mark.parametrize("name,ne", [("c5", 4), ("c2", 4)])
+def test_slab_pcg_single_rank_equals_plain(name, ne):
+    """Slab form of the inexact PCG (all-reduced scalars, dg_axpby updates) with
+    one rank: same iteration count and residual history as the library's pcg_solve, same solution."""
+    from paper_1612_04796_b200 import SlabDG
+    c = get_config(name, ne)
+    g = _gpu(c)
+    sd = SlabDG(c.ne, c.length, c.P, c.basis, c.penalty, c.overlap)
+    f = uniform_zero_mean(c.ndofs, 0)
+    fg = _t(f)
+    u_plain = torch.zeros_like(fg)
+    _, h_plain, ok = g.pcg_solve(u_plain, fg, rtol=1e-10, maxit=100)
+    assert ok
+    fl = sd.scatter_global(fg)
+    ul = torch.zeros_like(fl)
+    _, h_slab, ok2 = sd.pcg_solve(ul, fl, rtol=1e-10, maxit=100)
+    assert ok2 and len(h_slab) == len(h_plain)
+    assert np.allclose(h_slab, h_plain, rtol=1e-6)
+    assert _rel(_n(sd.gather_global(ul)), _n(u_plain)) <= 1e-8

@@ -95,6 +95,14 @@ class OracleLocal:
         uf.add_(torch.from_numpy(self.H.prolong(level, uc.numpy())))
         return uf
 
+    def apply(self, u, level, out):
+        out.copy_(torch.from_numpy(self.H.apply(level, u.numpy())))
+        return out
+
+    def axpby(self, y, a, x, b=1.0):
+        y.copy_(a * x if b == 0.0 else a * x + b * y)
+        return y
+
     def dot_range(self, x, y, count):
         return float(np.dot(x.numpy()[:count], y.numpy()[:count]))
 
@@ -140,7 +148,10 @@ def _worker(rank, world, port, case, out):
         iterates.append(sd.gather_global(ul).numpy().copy())
         r = sd.residual(ul, fl)
         norms.append(sd.dot(r, r))
-    out[rank] = (iterates, norms, sd.exchanges, sd.z0, sd.nzl)
+    nex = sd.exchanges
+    up = torch.zeros_like(fl)
+    _, hist, ok = sd.pcg_solve(up, fl, rtol=1e-9, maxit=40)
+    out[rank] = (iterates, norms, nex, sd.z0, sd.nzl, hist, ok, sd.gather_global(up).numpy().copy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -170,9 +181,16 @@ def test_two_rank_slab_vcycles_equal_single_domain_oracle(case):
         u = mg.vcycle(H, u, f)
         rn = mg.residual_norm(H, u, f) ** 2
         for r in range(world):
-            iterates, norms, nex, z0, nzl = out[r]
+            iterates, norms, nex, z0, nzl = out[r][:5]
             assert np.max(np.abs(iterates[k] - u)) <= 1e-12 * np.max(np.abs(u)), (case, r, k)
             assert abs(norms[k] - rn) <= 1e-9 * rn
+    # inexact PCG on slabs (all-reduced scalars) against the oracle's PCG on the whole mesh
+    x_ref, h_ref = mg.pcg(H, f, rtol=1e-9, maxit=40)
+    for r in range(world):
+        hist, ok, x = out[r][5], out[r][6], out[r][7]
+        assert ok and len(hist) == len(h_ref)
+        assert np.allclose(hist, h_ref, rtol=1e-6)
+        assert np.max(np.abs(x - x_ref)) <= 1e-8 * np.max(np.abs(x_ref))
     assert out[0][3] == 0 and out[1][3] == out[0][4]          # slabs are consecutive z ranges
     assert out[0][2] == out[1][2] > 0                         # both ranks issued the same exchanges
 
