@@ -125,6 +125,10 @@ __device__ __forceinline__ void eo17_afrag(const double *__restrict__ Daug, doub
   }
 }
 
+#ifndef PMG_APPLY17_THREADS
+#define PMG_APPLY17_THREADS 256     // CTA width of the n = 17 apply (2 CTAs per SM)
+#endif
+
 template <int DIR, bool FIRST>
 __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, double *V,
                                            const double *af, const unsigned short *cmap,
@@ -232,7 +236,7 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
 // NT = n (compile time, n = 2^l + 1 or 2), NC = (n + 1) / 2 the next-coarser n (fused restriction)
 // WIDE: 256-thread CTAs for n <= 9 when the whole mesh is one wave (latency-bound small meshes)
 template <int NT, bool WIDE = false>
-__global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WIDE ? 4 : 8) : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
+__global__ void __launch_bounds__(NT == 17 ? PMG_APPLY17_THREADS : ((NT <= 9 && !WIDE) ? 128 : 256), NT <= 9 ? (WIDE ? 4 : 8) : 2) k_apply_mma(LevelDev L, const double *__restrict__ u,
                                                       const double *__restrict__ T,
                                                       const double *__restrict__ f,
                                                       double *__restrict__ out,
@@ -362,28 +366,39 @@ __global__ void __launch_bounds__((NT <= 9 && !WIDE) ? 128 : 256, NT <= 9 ? (WID
     // out = f - M v (or M v), M = Mz (x) My (x) Mx; f loads batched for memory-level parallelism:
     // up to 10 f loads per thread in flight (the epilogue was a fifth of the kernel's time with 4)
     const long long g0 = (long long)e * n3;
+    constexpr int THR = NT == 17 ? PMG_APPLY17_THREADS : ((NT <= 9 && !WIDE) ? 128 : 256);
 #ifndef PMG_APPLY_UNR
-    constexpr int THR = (NT <= 9 && !WIDE) ? 128 : 256;
-    constexpr int UNR = NT == 17 ? 10 : (n3 + THR - 1) / THR;   // n = 17: 20 spills (measured 10 best)
+    constexpr int UNR = NT == 17 ? (THR == 256 ? 10 : 8) : (n3 + THR - 1) / THR;   // n = 17: 20 spills (measured 10 best)
 #else
     constexpr int UNR = PMG_APPLY_UNR;
 #endif
-    for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * blockDim.x) {
+    // node (i, j, k) of DOF t is tracked incrementally over the thread's DOFs t0 + q THR
+    // (THR = SK n^2 + SJ n + SI): two compare-and-carry steps instead of a division per DOF
+    constexpr int SI = THR % n, SJ = (THR / n) % n, SK = THR / n2;
+    for (int t0 = threadIdx.x; t0 < n3; t0 += UNR * THR) {
       double fv[UNR];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const int t = t0 + q * blockDim.x;
+        const int t = t0 + q * THR;
         fv[q] = (f && t < n3) ? __ldg(f + g0 + t) : 0.0;
       }
+      int i = t0 % n, j = (t0 / n) % n, k = t0 / n2;
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const int t = t0 + q * blockDim.x;
+        const int t = t0 + q * THR;
         if (t >= n3) break;
-        const int i = t % n, j = (t / n) % n, k = t / n2;
+        if constexpr (NT != 17) {        // n <= 9: the per-DOF division measured faster (0.109 vs 0.120 ms)
+          i = t % n; j = (t / n) % n; k = t / n2;
+        }
         const double v = ms[i] * ms[n + j] * ms[2 * n + k] * V[t];
         const double rr = f ? fv[q] - v : v;
         if (restrict_I) V[t] = rr;
         else out[g0 + t] = rr;
+        if constexpr (NT == 17) {
+          i += SI; j += SJ; k += SK;
+          if (i >= n) { i -= n; ++j; }
+          if (j >= n) { j -= n; ++k; }
+        }
       }
     }
     __syncthreads();
@@ -633,7 +648,7 @@ static int apply_grid(size_t sb, long long Ne) {
   static int occ = 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_mma<NT, WIDE>,
-                                                  (NT <= 9 && !WIDE) ? 128 : 256, sb);
+                                                  NT == 17 ? PMG_APPLY17_THREADS : ((NT <= 9 && !WIDE) ? 128 : 256), sb);
     occ = std::max(occ, 1);
   }
   return (int)std::min<long long>(Ne, (long long)occ * num_sms());
@@ -661,7 +676,7 @@ static void launch_apply_nt(const LevelDev &L, const double *u, const double *T,
     k_apply_mma<NT, true><<<apply_grid<NT, true>(sb, L.Ne), 256, sb, s>>>(L, u, T, f, out, I, fc);
     return;
   }
-  const int threads = NT <= 9 ? 128 : 256;
+  const int threads = NT == 17 ? PMG_APPLY17_THREADS : (NT <= 9 ? 128 : 256);
   k_apply_mma<NT, false><<<apply_grid<NT, false>(sb, L.Ne), threads, sb, s>>>(L, u, T, f, out, I, fc);
 }
 

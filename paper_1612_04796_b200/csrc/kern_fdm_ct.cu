@@ -384,11 +384,38 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
       // latency, bounds this phase — a row per warp left 32 - M0 lanes idle), padded plane stride
     const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
 #ifndef PMG_EXP_NOGATHER      // diagnostic: timing without the window gather (wrong results)
+#ifdef PMG_GATHER_DIV         // round-2b form: a division pair per node (~33 instructions per copy)
     for (int w = threadIdx.x; w < Mw; w += SH::THREADS) {
       const int bc = w / M0, a = w - bc * M0;
       const int c = bc / M1, b = bc - c * M1;
       cp_async8(X + a + M0 * b + S2 * c, r + xo[a] + yo[b] + zo[c]);
     }
+#else
+    // node (a, b, c) and its padded shared-memory slot are tracked incrementally over the thread's
+    // nodes w = tid + q THREADS (two compare-and-carry steps, no division); when the level's
+    // vector has < 2^31 entries the three offsets are summed in 32 bits (low words of the table)
+    constexpr int TH = SH::THREADS, DA = TH % M0, DB = (TH / M0) % M1, DC = TH / (M0 * M1);
+    constexpr int PAD = S2 - M0 * M1;
+    int a = threadIdx.x % M0, b = (threadIdx.x / M0) % M1, c = threadIdx.x / (M0 * M1);
+    int dst = a + M0 * b + S2 * c;
+    if ((long long)L.Ne * L.n * L.n * L.n < (1LL << 31)) {
+      const int *xi = reinterpret_cast<const int *>(xo), *yi = reinterpret_cast<const int *>(yo),
+                *zi = reinterpret_cast<const int *>(zo);
+      for (int w = threadIdx.x; w < Mw; w += TH) {
+        cp_async8(X + dst, r + (xi[2 * a] + yi[2 * b] + zi[2 * c]));
+        a += DA; b += DB; c += DC; dst += TH + DC * PAD;
+        if (a >= M0) { a -= M0; ++b; }
+        if (b >= M1) { b -= M1; ++c; dst += PAD; }
+      }
+    } else {
+      for (int w = threadIdx.x; w < Mw; w += TH) {
+        cp_async8(X + dst, r + xo[a] + yo[b] + zo[c]);
+        a += DA; b += DB; c += DC; dst += TH + DC * PAD;
+        if (a >= M0) { a -= M0; ++b; }
+        if (b >= M1) { b -= M1; ++c; dst += PAD; }
+      }
+    }
+#endif
 #else
     (void)xo; (void)yo; (void)zo;
     for (int w = threadIdx.x; w < S2 * M2; w += SH::THREADS) X[w] = 1.0;

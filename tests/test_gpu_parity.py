@@ -555,11 +555,11 @@ def test_slab_pcg_single_rank_equals_plain(name, ne):
     f = uniform_zero_mean(c.ndofs, 0)
     fg = _t(f)
     u_plain = torch.zeros_like(fg)
-    _, h_plain, ok = g.pcg_solve(u_plain, fg, rtol=1e-10, maxit=100)
+    _, h_plain, ok = g.pcg_solve(u_plain, fg, rtol=1e-10, maxit=300)
     assert ok
     fl = sd.scatter_global(fg)
     ul = torch.zeros_like(fl)
-    _, h_slab, ok2 = sd.pcg_solve(ul, fl, rtol=1e-10, maxit=100)
+    _, h_slab, ok2 = sd.pcg_solve(ul, fl, rtol=1e-10, maxit=300)
     assert ok2 and len(h_slab) == len(h_plain)
     assert np.allclose(h_slab, h_plain, rtol=1e-6)
     assert _rel(_n(sd.gather_global(ul)), _n(u_plain)) <= 1e-8
