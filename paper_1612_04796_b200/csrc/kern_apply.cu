@@ -194,19 +194,21 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
     tl += __shfl_xor_sync(0xffffffffu, tl, 2);
   };
   auto epilogue = [&](int tile, const double (&cE)[2], const double (&cO)[2], double tl, int ob) {
+    // dead slots (the last tile's 7 duplicates of column 288) run the same loads and only predicate
+    // the stores: no divergent region in the tile loop
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int slot = tile * 8 + 2 * t + j;
-      if (slot >= NCOL) continue;
+      const bool ok = slot < NCOL;
       double *vb = V + coloff(slot, cmap[slot]);
-      const double lo = cE[j] + cO[j], hi = cE[j] - cO[j];
-      if (FIRST) { vb[g * SO] = lo; vb[(n - 1 - g) * SO] = hi; }
-      else { vb[g * SO] += lo; vb[(n - 1 - g) * SO] += hi; }
+      double lo = cE[j] + cO[j], hi = cE[j] - cO[j];
+      if (!FIRST) { lo += vb[g * SO]; hi += vb[(n - 1 - g) * SO]; }
+      if (ok) { vb[g * SO] = lo; vb[(n - 1 - g) * SO] = hi; }
     }
-    if (t == 0 && tile * 8 + g < NCOL) {
+    {
       double *vb = V + ob + H * SO;
-      if (FIRST) *vb = tl;
-      else *vb += tl;
+      if (!FIRST) tl += *vb;
+      if (t == 0 && tile * 8 + g < NCOL) *vb = tl;
     }
   };
   // software pipelined: the DMMAs of tile i + nw are issued before the epilogue of tile i
@@ -216,13 +218,13 @@ __device__ __forceinline__ void apply_eo17(const double *U, const double *Cfd, d
   compute(tile, cE0, cO0, tl0, ob0);
   for (;;) {
     const int t1 = tile + nw;
+    // (no __syncwarp: U and Cf are read-only in a pass and every V address is read and written
+    // by one lane only)
     if (t1 < NT) compute(t1, cE1, cO1, tl1, ob1);
-    __syncwarp();
     epilogue(tile, cE0, cO0, tl0, ob0);
     if (t1 >= NT) break;
     const int t2 = t1 + nw;
     if (t2 < NT) compute(t2, cE0, cO0, tl0, ob0);
-    __syncwarp();
     epilogue(t1, cE1, cO1, tl1, ob1);
     if (t2 >= NT) break;
     tile = t2;
