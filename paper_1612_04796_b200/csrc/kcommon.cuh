@@ -515,6 +515,110 @@ __device__ __forceinline__ bool fdm_z_fused(double *X, const Blk &B, const doubl
   return false;
 }
 
+
+// ---- face traces of one element held in shared memory ---------------------------------------
+// Eq. 7's rank-2 face couplings need, per face point, the value and the
+// (2/Delta)-scaled normal derivative of the element's polynomial on its left / right face:
+//   rv = sum_q phi_q(+1) u_q, rder = sum_q phi'_q(+1) u_q, lv, lder likewise at -1.
+// The node set is reflection symmetric, phi_q(-1) = phi_{n-1-q}(+1) and phi'_q(-1) =
+// -phi'_{n-1-q}(+1), so with s_q = u_q + u_{n-1-q}, d_q = u_q - u_{n-1-q} (q < n/2)
+//   rv = E + O, lv = E - O, rder = G + F, lder = F - G,
+//   E = sum cE_q s_q + a_mid u_mid, O = sum cO_q d_q, G = sum gE_q s_q + ap_mid u_mid, F = sum gO_q d_q
+// — 4 FMAs per node PAIR instead of 4 per node, one 32-byte coefficient entry per pair.  On GLL
+// nodes phi_q(+-1) is a unit vector and the value traces are the face nodes themselves.
+// Table per direction d (TRACE_TAB(n) doubles, 16-byte aligned): {cE, cO, gE, gO} for q < n/2,
+// then {a_mid, ap_mid, 0, 0}; tab[3 TRACE_TAB] = 1.0 when the basis is nodal on the faces.
+#define PMG_MAX_N 33                      // P <= 32 (dg_setup)
+__host__ __device__ constexpr int trace_tab_len(int n) { return 4 * (n / 2 + 1); }
+
+__device__ __forceinline__ void stage_trace_tab(const LevelDev &L, double *tab) {
+  const int n = L.n, h = n / 2, len = trace_tab_len(n);
+  for (int idx = threadIdx.x; idx < 3 * (h + 1); idx += blockDim.x) {
+    const int d = idx / (h + 1), q = idx - d * (h + 1);
+    const double *tr = L.tr[d];
+    double *e = tab + d * len + 4 * q;
+    if (q < h) {
+      const double a = tr[q], ar = tr[n - 1 - q], ap = tr[n + q], apr = tr[n + n - 1 - q];
+      e[0] = 0.5 * (a + ar); e[1] = 0.5 * (a - ar); e[2] = 0.5 * (ap + apr); e[3] = 0.5 * (ap - apr);
+    } else {
+      const bool odd = (n & 1) != 0;
+      e[0] = odd ? tr[h] : 0.0; e[1] = odd ? tr[n + h] : 0.0; e[2] = 0.0; e[3] = 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    bool nodal = L.tr[0][n - 1] == 1.0;
+    for (int q = 0; q + 1 < n; ++q) nodal = nodal && L.tr[0][q] == 0.0;
+    tab[3 * len] = nodal ? 1.0 : 0.0;
+  }
+}
+
+// one face point: the line of n nodes lo[0], lo[stride], ..., tabd = the direction's table
+template <int NT>
+__device__ __forceinline__ void trace_point(const double *lo, int stride, int nrt, const double *tabd,
+                                            bool nodal, double &lv, double &lder, double &rv,
+                                            double &rder) {
+  const int n = NT > 0 ? NT : nrt;
+  const int h = n / 2;
+  const double2 *c2 = reinterpret_cast<const double2 *>(tabd);
+  const double *hi = lo + (n - 1) * stride;
+  double E = 0, O = 0, G = 0, F = 0;
+  if (nodal) {
+#pragma unroll
+    for (int q = 0; q < (NT > 0 ? NT / 2 : h); ++q) {
+      const double u1 = lo[q * stride], u2 = hi[-q * stride];
+      const double2 g = c2[2 * q + 1];
+      G = fma(g.x, u1 + u2, G);
+      F = fma(g.y, u1 - u2, F);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < (NT > 0 ? NT / 2 : h); ++q) {
+      const double u1 = lo[q * stride], u2 = hi[-q * stride];
+      const double sq = u1 + u2, dq = u1 - u2;
+      const double2 c = c2[2 * q], g = c2[2 * q + 1];
+      E = fma(c.x, sq, E);
+      O = fma(c.y, dq, O);
+      G = fma(g.x, sq, G);
+      F = fma(g.y, dq, F);
+    }
+  }
+  if (n & 1) {
+    const double um = lo[h * stride];
+    const double2 m = c2[2 * h];
+    E = fma(m.x, um, E);
+    G = fma(m.y, um, G);
+  }
+  lv = nodal ? lo[0] : E - O;
+  lder = F - G;
+  rv = nodal ? hi[0] : E + O;
+  rder = G + F;
+}
+
+// traces of face point t in [0, 3 n^2) of the element at U (shared or global memory) -> Te
+template <int NT>
+__device__ __forceinline__ void elem_trace_item(const double *U, const double *tab, int nrt, int t,
+                                                double *Te) {
+  const int n = NT > 0 ? NT : nrt;
+  const int n2 = n * n, len = trace_tab_len(n);
+  const int d = t / n2, p = t - d * n2;
+  const int p1 = p / n, p0 = p - p1 * n;
+  int base, stride;
+  if (d == 0) { base = n * p; stride = 1; }
+  else if (d == 1) { base = p0 + n2 * p1; stride = n; }
+  else { base = p; stride = n2; }
+  double lv, lder, rv, rder;
+  trace_point<NT>(U + base, stride, n, tab + d * len, tab[3 * len] != 0.0, lv, lder, rv, rder);
+  double *Td = Te + d * 4 * n2;
+  Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+}
+
+// all threads of the CTA; U: the element (n^3, x fastest) in shared memory; Te: its 12 n^2 traces
+template <int NT>
+__device__ __forceinline__ void elem_traces(const double *U, const double *tab, int nrt, double *Te) {
+  const int n = NT > 0 ? NT : nrt;
+  for (int t = threadIdx.x; t < 3 * n * n; t += blockDim.x) elem_trace_item<NT>(U, tab, n, t, Te);
+}
+
 // ---- building blocks of the subdomain solve (shared by the one-shot and persistent kernels)
 // gather offsets of subdomain e: global address of window node (a,b,c) = xo[a] + yo[b] + zo[c]
 __device__ __forceinline__ void fdm_offsets(const LevelDev &L, int e, long long *offs) {

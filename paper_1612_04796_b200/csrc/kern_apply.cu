@@ -17,25 +17,11 @@ __global__ void k_traces(LevelDev L, const double *__restrict__ u, double *__res
   const double *ue = u + (long long)e * n3;
   double *Te = T + (long long)e * 12 * n2;
   // 2D grid: blockIdx.y splits the 3 n^2 face points (large elements fill the GPU)
-  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < 3 * n2; t += gridDim.y * blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = L.tr[d];
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int i = 0; i < n; ++i) {
-      const double v = __ldg(ue + base + i * stride);
-      rv += tr[i] * v;
-      rder += tr[n + i] * v;
-      lv += tr[2 * n + i] * v;
-      lder += tr[3 * n + i] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
+  __shared__ __align__(16) double tab[3 * trace_tab_len(PMG_MAX_N) + 2];
+  stage_trace_tab(L, tab);
+  __syncthreads();
+  for (int t = blockIdx.y * blockDim.x + threadIdx.x; t < 3 * n2; t += gridDim.y * blockDim.x)
+    elem_trace_item<0>(ue, tab, n, t, Te);
 }
 
 // Operator apply v = A u (Eq. 7) or residual r = f - A u (Eq. 8), sum-factorised per element.
@@ -554,8 +540,8 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
                                                    double *__restrict__ T) {
   extern __shared__ double sm[];
   const int n = L.n, n2 = n * n, n3 = n2 * n;
-  double *Us = sm, *trs = sm + n3 + 2;
-  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * n);
+  double *Us = sm, *tab = sm + ((n3 + 3) & ~1);
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(tab + 3 * trace_tab_len(n) + 2);
   const int e = blockIdx.x;
   const BulkPlan bp = bulk_plan(Us, u + (long long)e * n3, n3, u + (long long)L.Ne * n3);
   double *U = bp.ptr;
@@ -568,30 +554,14 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
   } else {
     stage(U, u + (long long)e * n3, n3);
   }
-  for (int d = 0; d < 3; ++d) stage(trs + d * 4 * n, L.tr[d], 4 * n);
+  stage_trace_tab(L, tab);
   cp_async_wait_all();
   __syncthreads();
   if (bp.bytes) mbar_wait(mbar, 0);
   double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int i = 0; i < n; ++i) {
-      const double v = U[base + i * stride];
-      rv += tr[i] * v;
-      rder += tr[n + i] * v;
-      lv += tr[2 * n + i] * v;
-      lder += tr[3 * n + i] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
+  if (n == 17) elem_traces<17>(U, tab, n, Te);
+  else if (n == 9) elem_traces<9>(U, tab, n, Te);
+  else elem_traces<0>(U, tab, n, Te);
 }
 
 }  // namespace
@@ -599,7 +569,7 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_traces(const LevelDev &L, const double *u, double *T, cudaStream_t s) {
   const int n = L.n;
-  const size_t sb = sizeof(double) * ((size_t)n * n * n + 2 + 12 * n + 2);
+  const size_t sb = sizeof(double) * ((size_t)n * n * n + 4 + 3 * trace_tab_len(n) + 2 + 2);
   if (n <= 20) {
     static size_t configured = 0;
     if (sb > 48 * 1024 && sb > configured) {

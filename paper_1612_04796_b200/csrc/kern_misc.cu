@@ -72,31 +72,10 @@ __global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__re
   }
   if (!TR) return;
   // fused trace pass of the following residual: face values / derivatives of the new u
-  const int n2 = n * n;
-  double *trs = sm + n3;
-  for (int d = 0; d < 3; ++d)
-    for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) trs[d * 4 * n + i] = L.tr[d][i];
+  double *tab = sm + ((n3 + 1) & ~1);
+  stage_trace_tab(L, tab);
   __syncthreads();
-  double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int i = 0; i < n; ++i) {
-      const double v = sm[base + i * stride];
-      rv += tr[i] * v;
-      rder += tr[n + i] * v;
-      lv += tr[2 * n + i] * v;
-      lder += tr[3 * n + i] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
+  elem_traces<0>(sm, tab, n, T + (long long)e * 12 * n * n);
 }
 
 // Row fold (Eq. 10): a warp folds whole x-rows of the element.  Lane a of a
@@ -131,6 +110,7 @@ __global__ void __launch_bounds__(256, 4) k_fold4(LevelDev L, const double *__re
 #pragma unroll
     for (int o = 0; o < 3; ++o)
       sb[d][o] = wrap(ec[d] + o - 1, edim[d]) * (int)(d == 0 ? Mw : (d == 1 ? Mw * L.nx : Mw * L.nx * L.ny));
+  if (TR) stage_trace_tab(L, sm + ((n3 + 1) & ~1));    // read after the post-fold barrier
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int rpw = 32 / mx;                                  // rows per warp instruction (>= 1)
   const int sr = lane / mx, a = lane - sr * mx;
@@ -199,30 +179,8 @@ __global__ void __launch_bounds__(256, 4) k_fold4(LevelDev L, const double *__re
   if (!TR) return;
   __syncthreads();
   // fused trace pass of the following residual: face values / derivatives of the new u
-  double *trs = sm + n3;
-  for (int d = 0; d < 3; ++d)
-    for (int t = threadIdx.x; t < 4 * n; t += blockDim.x) trs[d * 4 * n + t] = L.tr[d][t];
-  __syncthreads();
-  double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int q = 0; q < n; ++q) {
-      const double v = sm[base + q * stride];
-      rv += tr[q] * v;
-      rder += tr[n + q] * v;
-      lv += tr[2 * n + q] * v;
-      lder += tr[3 * n + q] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
+  // (even/odd form, kcommon.cuh); the table was staged before the fold loop
+  elem_traces<NT>(sm, sm + ((n3 + 1) & ~1), n, T + (long long)e * 12 * n2);
 }
 
 // Small elements (n = 3, 5): EPB elements per 256-thread CTA, one thread per DOF, same fixed
@@ -235,14 +193,12 @@ __global__ void __launch_bounds__(256) k_fold_small(LevelDev L, const double *__
                                                   double *__restrict__ T) {
   constexpr int n = NT, n2 = n * n, n3 = n2 * n;
   __shared__ double sm[EPB * n3];
-  __shared__ double trs[12 * n];
+  __shared__ __align__(16) double trs[3 * trace_tab_len(n) + 2];   // even/odd trace table
   const int mx = L.m[0], my = L.m[1];
   const long long Zs = L.Mw;
   const int le = threadIdx.x / n3, t = threadIdx.x - le * n3;
   const int e = blockIdx.x * EPB + le;
-  if (TR)
-    for (int d = 0; d < 3; ++d)
-      for (int i = threadIdx.x; i < 4 * n; i += blockDim.x) trs[d * 4 * n + i] = L.tr[d][i];
+  if (TR) stage_trace_tab(L, trs);
   if (le < EPB && e < L.Ne) {
     const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
     const int edim[3] = {L.nx, L.ny, L.nz};
@@ -289,25 +245,7 @@ __global__ void __launch_bounds__(256) k_fold_small(LevelDev L, const double *__
     const int lb = w / (3 * n2), r = w - lb * 3 * n2;
     const int eb = blockIdx.x * EPB + lb;
     if (eb >= L.Ne) break;
-    const int d = r / n2, p = r - d * n2;
-    const int p0 = p % n, p1 = p / n;
-    int base, stride;
-    if (d == 0) { base = n * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = n; }
-    else { base = p0 + n * p1; stride = n2; }
-    const double *tr = trs + d * 4 * n;
-    const double *ue = sm + lb * n3;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-#pragma unroll
-    for (int q = 0; q < n; ++q) {
-      const double vv = ue[base + q * stride];
-      rv += tr[q] * vv;
-      rder += tr[n + q] * vv;
-      lv += tr[2 * n + q] * vv;
-      lder += tr[3 * n + q] * vv;
-    }
-    double *Td = T + (long long)eb * 12 * n2 + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
+    elem_trace_item<NT>(sm + lb * n3, trs, n, r, T + (long long)eb * 12 * n2);
   }
 }
 
@@ -877,7 +815,7 @@ cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero
     // row fold (k_fold4): window rows fit a warp, the element fits shared memory for the traces
     const int n = L.n;
     const bool merged = 2 * L.no[0] <= n && 2 * L.no[1] <= n && 2 * L.no[2] <= n;
-    const size_t sb4 = T ? sizeof(double) * ((size_t)n * n * n + 12 * n) : 0;
+    const size_t sb4 = T ? sizeof(double) * ((size_t)n * n * n + 1 + 3 * trace_tab_len(n) + 1) : 0;
 #define PMG_FOLD4(NN, MM)                                                                       \
   do {                                                                                          \
     static bool cfg4 = false;                                                                   \

@@ -26,8 +26,9 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_P
   const int c3p = (c3 + 3) & ~1;                // staging capacities (16-byte aligned regions)
   const int ap = (max(c3p, nf * nf * nc) + 1) & ~1;
   double *Ucs = sm, *T2 = sm, *Us = sm + ap;
-  double *T1 = Us + ((n3 + 3) & ~1), *trs = T1 + nf * nc * nc;
-  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(trs + 12 * nf);
+  double *T1 = Us + ((n3 + 3) & ~1);
+  double *trs = T1 + ((nf * nc * nc + 1) & ~1);     // even/odd trace table (16-byte aligned)
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(T1 + nf * nc * nc + 12 * nf);
   const int e = blockIdx.x;
   const BulkPlan bc = bulk_plan(Ucs, uc + (long long)e * c3, c3, uc + (long long)L.Ne * c3);
   const BulkPlan bf = bulk_plan(Us, uf + (long long)e * n3, n3, uf + (long long)L.Ne * n3);
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_P
   }
   if (!bc.bytes) stage(Uc, uc + (long long)e * c3, c3);
   if (!bf.bytes) stage(U, uf + (long long)e * n3, n3);
-  for (int d = 0; d < 3; ++d) stage(trs + d * 4 * nf, L.tr[d], 4 * nf);
+  stage_trace_tab(L, trs);
   cp_async_wait_all();
   __syncthreads();
   if (bc.bytes || bf.bytes) mbar_wait(mbar, 0);
@@ -57,26 +58,7 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_P
   mma_lines_gen<2, KSMAX>(T2, B2, px, acc); __syncthreads();
   double *ue = uf + (long long)e * n3;
   for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
-  double *Te = T + (long long)e * 12 * n2;
-  for (int t = threadIdx.x; t < 3 * n2; t += blockDim.x) {
-    const int d = t / n2, p = t - d * n2;
-    const int p0 = p % nf, p1 = p / nf;
-    int base, stride;
-    if (d == 0) { base = nf * p0 + n2 * p1; stride = 1; }
-    else if (d == 1) { base = p0 + n2 * p1; stride = nf; }
-    else { base = p0 + nf * p1; stride = n2; }
-    const double *tr = trs + d * 4 * nf;
-    double lv = 0, lder = 0, rv = 0, rder = 0;
-    for (int i = 0; i < nf; ++i) {
-      const double v = U[base + i * stride];
-      rv += tr[i] * v;
-      rder += tr[nf + i] * v;
-      lv += tr[2 * nf + i] * v;
-      lder += tr[3 * nf + i] * v;
-    }
-    double *Td = Te + d * 4 * n2;
-    Td[p] = lv; Td[n2 + p] = lder; Td[2 * n2 + p] = rv; Td[3 * n2 + p] = rder;
-  }
+  elem_traces<0>(U, trs, nf, T + (long long)e * 12 * n2);
 }
 
 // Residual restriction f_c = I^T r_f per element (Alg. 1 l.292).
