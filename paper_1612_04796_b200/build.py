@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmgdg.so")
-SOURCES = ["api.cu", "kern_fdm.cu", "kern_fdm_ct.cu", "kern_apply.cu", "kern_apply33.cu", "kern_xfer.cu", "kern_global.cu", "kern_misc.cu",
+SOURCES = ["api.cu", "kern_fdm.cu", "kern_fdm_ct.cu", "kern_fdm_dl.cu", "kern_apply.cu", "kern_apply33.cu", "kern_xfer.cu", "kern_global.cu", "kern_misc.cu",
            "setup.cpp", "probe.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

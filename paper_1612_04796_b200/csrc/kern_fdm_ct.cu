@@ -93,11 +93,11 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
   // z fastest), so the B loads need pi(g) mod 4 distinct over each half-warp's four g and the C
   // stores need pi(2t + j) mod 4 distinct over t: the identity order made the stores of lanes
   // (g, t) and (g, t + 2) collide (ncu: 31 % of the kernel's shared-memory wavefronts).
-#ifdef PMG_EOC_PERM            // measured neutral (fdm@l4 1.229 vs 1.226 ms): the stores are not the limiter
-  auto pi = [](int c) { return c ^ ((c >> 2) & 1); };
-#else
-  auto pi = [](int c) { return c; };
-#endif
+  // Measured: 13^3 windows 0.193 -> 0.185 ms per cycle (that kernel keeps the shared-memory pipe
+  // ~70 % busy), c5's shapes -0.4 %; neutral to +0.3 % on 23^3 (1.2275 -> 1.2314: the stores are not
+  // its limiter), which keeps the identity order.
+  constexpr bool PERM = !(SH::template m<0>() == 23 && SH::template m<1>() == 23 && SH::template m<2>() == 23);
+  auto pi = [](int c) { return PERM ? (c ^ ((c >> 2) & 1)) : c; };
   Col cb, c0, c1;
   col_init(warp * 8 + pi(g), cb);
   col_init(warp * 8 + pi(2 * t), c0);
@@ -633,6 +633,7 @@ bool fdm_eoc_launch(const LevelDev &L, const double *r, double *Z, int color, do
 #ifdef PMG_NO_EOC
   return false;
 #endif
+  if (color < 0 && fdm_dl_launch(L, r, Z, s)) return true;   // small windows: FP64-FMA line kernel
   const int grid = color >= 0 ? L.Ne / 8 : L.Ne;
 #define PMG_EOC_CASE(a, b, c)                                    \
   if (L.m[0] == a && L.m[1] == b && L.m[2] == c) {              \

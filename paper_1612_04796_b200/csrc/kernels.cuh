@@ -42,6 +42,8 @@ cudaError_t launch_fdm_global(const LevelDev &L, const double *r, double *X, dou
                               cudaStream_t s);
 cudaError_t launch_apply_global(const LevelDev &L, const double *u, const double *T, const double *f,
                                 double *out, double *Cb, double *V, cudaStream_t s);
+// small windows (m <= 15): thread-per-line FP64-FMA fast diagonalisation (kern_fdm_dl.cu)
+bool fdm_dl_launch(const LevelDev &L, const double *r, double *Z, cudaStream_t s);
 bool fdm_mma_ok(const LevelDev &L);
 // P = 32 (n = 33) apply / residual: two slab kernels with even/odd DMMA line GEMMs in shared
 // memory (kern_apply33.cu); V: Ne * 33^3 scratch (x + z contributions)
