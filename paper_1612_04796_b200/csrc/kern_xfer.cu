@@ -15,13 +15,16 @@ namespace {
 #ifndef PMG_PT_MINB
 #define PMG_PT_MINB 3
 #endif
-template <int KSMAX>
-__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_PT_MINB) k_prolong_traces(LevelDev L, int nc, const double *__restrict__ I,
+// NF, NC > 0: both extents compile-time (the 9 -> 17 and 5 -> 9 transfers of every configuration):
+// one tile variant per pass is inlined, strides and trip counts fold to constants
+template <int KSMAX, int NF = 0, int NCT = 0>
+__global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_PT_MINB) k_prolong_traces(LevelDev L, int ncr, const double *__restrict__ I,
                                                         const double *__restrict__ uc,
                                                         double *__restrict__ uf,
                                                         double *__restrict__ T) {
   extern __shared__ double sm[];
-  const int nf = L.n, n2 = nf * nf, n3 = n2 * nf;
+  const int nf = NF > 0 ? NF : L.n, n2 = nf * nf, n3 = n2 * nf;
+  const int nc = NCT > 0 ? NCT : ncr;
   const int c3 = nc * nc * nc;
   const int c3p = (c3 + 3) & ~1;                // staging capacities (16-byte aligned regions)
   const int ap = (max(c3p, nf * nf * nc) + 1) & ~1;
@@ -51,14 +54,20 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_P
   const Blk BF = {{nf, nf, nf}, {1, nf, n2}};
   const LineSpec px = {nf, nc, I, nc, 1, nullptr, 0, 0, 0, 0};   // A[o][k] = I[o*nc + k]
   EpiStore s1{T1, B1};
-  mma_lines_gen<0, KSMAX>(Uc, BC, px, s1); __syncthreads();
   EpiStore s2{T2, B2};
-  mma_lines_gen<1, KSMAX>(T1, B1, px, s2); __syncthreads();
   EpiAcc acc{U, BF, false};
-  mma_lines_gen<2, KSMAX>(T2, B2, px, acc); __syncthreads();
+  if constexpr (NF > 0) {
+    mma_lines_ct<0, NF, NCT>(Uc, BC, px, s1); __syncthreads();
+    mma_lines_ct<1, NF, NCT>(T1, B1, px, s2); __syncthreads();
+    mma_lines_ct<2, NF, NCT>(T2, B2, px, acc); __syncthreads();
+  } else {
+    mma_lines_gen<0, KSMAX>(Uc, BC, px, s1); __syncthreads();
+    mma_lines_gen<1, KSMAX>(T1, B1, px, s2); __syncthreads();
+    mma_lines_gen<2, KSMAX>(T2, B2, px, acc); __syncthreads();
+  }
   double *ue = uf + (long long)e * n3;
   for (int t = threadIdx.x; t < n3; t += blockDim.x) ue[t] = U[t];
-  elem_traces<0>(U, trs, nf, T + (long long)e * 12 * n2);
+  elem_traces<NF>(U, trs, nf, T + (long long)e * 12 * n2);
 }
 
 // Residual restriction f_c = I^T r_f per element (Alg. 1 l.292).
@@ -104,6 +113,8 @@ static void configure_smem() {
   cudaFuncSetAttribute(k_prolong_traces<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_prolong_traces<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_prolong_traces<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_prolong_traces<8, 17, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_prolong_traces<2, 9, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 
 static size_t prolong_traces_smem(int nf, int nc) {
@@ -121,6 +132,11 @@ cudaError_t launch_prolong_traces(const LevelDev &Lf, int nc, const double *I, c
                                   double *uf, double *T, cudaStream_t s) {
   configure_smem();
   const size_t sb = prolong_traces_smem(Lf.n, nc);
+#ifndef PMG_PT_GENERIC
+  if (Lf.n == 17 && nc == 9) k_prolong_traces<8, 17, 9><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);
+  else if (Lf.n == 9 && nc == 5) k_prolong_traces<2, 9, 5><<<Lf.Ne, 128, sb, s>>>(Lf, nc, I, uc, uf, T);
+  else
+#endif
   if (Lf.n >= 17) k_prolong_traces<8><<<Lf.Ne, 256, sb, s>>>(Lf, nc, I, uc, uf, T);   // big blocks: 8 warps
   else if (((nc + 3) >> 2) <= 2) k_prolong_traces<2><<<Lf.Ne, 128, sb, s>>>(Lf, nc, I, uc, uf, T);
   else if (((nc + 3) >> 2) <= 4) k_prolong_traces<4><<<Lf.Ne, 128, sb, s>>>(Lf, nc, I, uc, uf, T);
