@@ -353,7 +353,11 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
     stage(lam[d], L.lam[d], mm[d]);
     stage(W[d], L.W[d], mm[d]);
   }
+#ifdef PMG_FDM_REVERSE         // diagnostic: walk the subdomains backwards (tail of r still in L2)
+  int e = color >= 0 ? blockIdx.x : gridDim.x - 1 - blockIdx.x;
+#else
   int e = blockIdx.x;
+#endif
   if (color >= 0) {       // subdomain bx of parity class `color` (2x2x2 colouring)
     const int hx = L.nx >> 1, hy = L.ny >> 1;
     const int bx = e % hx, by = (e / hx) % hy, bz = e / (hx * hy);
