@@ -544,7 +544,11 @@ __global__ void __launch_bounds__(256) k_traces_sm(LevelDev L, const double *__r
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(tab + 3 * trace_tab_len(n) + 2);
   // elements are walked backwards: the fold's last writes of u are still in L2, and the traces of
   // the FIRST elements are written last, where the following apply starts (apply@l4 0.602 -> 0.591)
+#ifdef PMG_TRACES_FORWARD
+  const int e = blockIdx.x;
+#else
   const int e = gridDim.x - 1 - blockIdx.x;
+#endif
   const BulkPlan bp = bulk_plan(Us, u + (long long)e * n3, n3, u + (long long)L.Ne * n3);
   double *U = bp.ptr;
   if (bp.bytes) {

@@ -90,8 +90,11 @@ __global__ void __launch_bounds__(256, 4) k_fold2(LevelDev L, const double *__re
 // thread instructions per DOF, 27 mostly predicated-off loads), and RB rows per warp are in
 // flight at once.  32 / m_x rows share a warp when they fit (n = 9: two rows of 13 lanes).
 // Fixed summation order -> deterministic.  TR: face traces of the new u from shared memory.
+#ifndef PMG_FOLD4_MINB
+#define PMG_FOLD4_MINB 4
+#endif
 template <int NT, bool TR, bool MERGED>
-__global__ void __launch_bounds__(256, 4) k_fold4(LevelDev L, const double *__restrict__ Z,
+__global__ void __launch_bounds__(256, PMG_FOLD4_MINB) k_fold4(LevelDev L, const double *__restrict__ Z,
                                                   double *__restrict__ u, int zero,
                                                   double *__restrict__ T) {
   extern __shared__ double sm[];          // TR: the folded element (n^3) + trace table (12 n)
@@ -100,7 +103,11 @@ __global__ void __launch_bounds__(256, 4) k_fold4(LevelDev L, const double *__re
   const int mx = L.m[0], my = L.m[1];
   const int no0 = L.no[0], no1 = L.no[1], no2 = L.no[2];
   const long long Mw = L.Mw;
+#ifdef PMG_FOLD_REVERSE        // diagnostic: walk the elements backwards (the tail of Z is still in L2)
+  const int e = gridDim.x - 1 - blockIdx.x;
+#else
   const int e = blockIdx.x;
+#endif
   const int ec[3] = {e % L.nx, (e / L.nx) % L.ny, e / (L.nx * L.ny)};
   const int edim[3] = {L.nx, L.ny, L.nz};
   // all offsets are 32-bit element indices into Z (the launcher checks Ne * Mw < 2^31)
