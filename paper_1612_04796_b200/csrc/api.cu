@@ -423,7 +423,8 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
     } else {
       if (c->lev[l].o_x1)
         LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong_global(d, nc, Il, U[l - 1], U[l],
-                                       wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s));
+                                       wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s,
+                                       wsp<double>(c, c->lev[l].o_r)));    // r_l is dead here (scratch)
       else
         LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, nc, Il, U[l - 1], U[l], s));   // l.299
     }

@@ -58,7 +58,7 @@ cudaError_t launch_apply33(const LevelDev &L, const double *u, const double *T, 
 cudaError_t launch_restrict_global(const LevelDev &Lf, int nc, const double *I, const double *rf,
                                    double *fc, double *X1, double *X2, cudaStream_t s);
 cudaError_t launch_prolong_global(const LevelDev &Lf, int nc, const double *I, const double *uc,
-                                  double *uf, double *X1, double *X2, cudaStream_t s);
+                                  double *uf, double *X1, double *X2, cudaStream_t s, double *S = nullptr);
 // Colored Schwarz step: 8 launches (parity classes of the element coordinates); same-colour
 // windows are node-disjoint, so each subdomain adds W du_s straight into u (no Z, no fold);
 // deterministic (fixed colour order).  Needs even n_e and 2 n_o <= n in every direction.
