@@ -67,6 +67,16 @@ __device__ __forceinline__ void prefetch_l2(const void *src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// L2 prefetch of `count` doubles at `src` (8-byte aligned): the 16-byte aligned interior of the range.
+// Kernels whose CTAs start with a cold read of one contiguous block per element issue this for the
+// element a fixed number of CTAs ahead, so that the later CTA's loads are L2 hits.
+__device__ __forceinline__ void prefetch_l2_doubles(const double *src, long long count) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(src);
+  const unsigned skip = (a & 15) ? 1 : 0;
+  const long long bytes = ((count - skip) * 8) & ~15ll;
+  if (bytes > 0) prefetch_l2(src + skip, (unsigned)bytes);
+}
+
 // Plan a TMA copy of `count` doubles at `src` (8-byte aligned) into the 16-byte aligned staging
 // area `buf` (capacity count + 2): copies the 16-byte aligned superset; returns the pointer to
 // the first element inside `buf`, sets *bytes (0 if the superset would leave [src_base, src_end)).

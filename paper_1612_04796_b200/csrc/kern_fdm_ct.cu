@@ -370,6 +370,18 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
 #else
 #define PMG_PH(i)
 #endif
+  // Large levels (vector > 64 MB, i.e. not L2 resident): the r block of the subdomain 3/4 of a
+  // resident wave ahead is prefetched into L2, so that CTA's window gather (13 % of the kernel,
+  // exposed HBM latency) hits L2: c3 fdm@l4 1.227 -> 1.186 ms per cycle (distances 100-370 within
+  // 0.3 % of each other, 444 and 592 lose the gain)
+#ifndef PMG_FDM_PREFETCH
+#define PMG_FDM_PREFETCH 222
+#endif
+  if (PMG_FDM_PREFETCH > 0 && threadIdx.x == 0 && color < 0) {
+    const long long n3 = (long long)L.n * L.n * L.n;
+    const long long en = (long long)e + PMG_FDM_PREFETCH;
+    if (en < L.Ne && L.Ne * n3 > (8ll << 20)) prefetch_l2_doubles(r + en * n3, n3);
+  }
   fdm_offsets(L, e, offs);
   __syncthreads();
 #ifdef PMG_GATHER_ROWS

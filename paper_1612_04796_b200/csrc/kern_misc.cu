@@ -117,6 +117,12 @@ __global__ void __launch_bounds__(256, PMG_FOLD4_MINB) k_fold4(LevelDev L, const
 #pragma unroll
     for (int o = 0; o < 3; ++o)
       sb[d][o] = wrap(ec[d] + o - 1, edim[d]) * (int)(d == 0 ? Mw : (d == 1 ? Mw * L.nx : Mw * L.nx * L.ny));
+#ifdef PMG_FOLD_PREFETCH        // diagnostic: L2 prefetch of the Z and u blocks of the element that many CTAs ahead
+  if (threadIdx.x == 0 && (long long)e + PMG_FOLD_PREFETCH < L.Ne && (long long)L.Ne * n3 > (8ll << 20)) {
+    prefetch_l2_doubles(Z + ((long long)e + PMG_FOLD_PREFETCH) * Mw, Mw);
+    if (!zero) prefetch_l2_doubles(u + ((long long)e + PMG_FOLD_PREFETCH) * n3, n3);
+  }
+#endif
   if (TR) stage_trace_tab(L, sm + ((n3 + 1) & ~1));    // read after the post-fold barrier
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int rpw = 32 / mx;                                  // rows per warp instruction (>= 1)

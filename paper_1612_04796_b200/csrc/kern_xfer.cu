@@ -33,6 +33,10 @@ __global__ void __launch_bounds__(KSMAX <= 4 ? 128 : 256, KSMAX <= 4 ? 8 : PMG_P
   double *trs = T1 + ((nf * nc * nc + 1) & ~1);     // even/odd trace table (16-byte aligned)
   unsigned long long *mbar = reinterpret_cast<unsigned long long *>(T1 + nf * nc * nc + 12 * nf);
   const int e = blockIdx.x;
+#ifdef PMG_PT_PREFETCH          // diagnostic: L2 prefetch of the fine block of the element that many CTAs ahead
+  if (threadIdx.x == 0 && (long long)e + PMG_PT_PREFETCH < L.Ne && (long long)L.Ne * n3 > (8ll << 20))
+    prefetch_l2_doubles(uf + ((long long)e + PMG_PT_PREFETCH) * n3, n3);
+#endif
   const BulkPlan bc = bulk_plan(Ucs, uc + (long long)e * c3, c3, uc + (long long)L.Ne * c3);
   const BulkPlan bf = bulk_plan(Us, uf + (long long)e * n3, n3, uf + (long long)L.Ne * n3);
   double *Uc = bc.ptr, *U = bf.ptr;
