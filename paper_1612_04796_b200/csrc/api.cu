@@ -337,6 +337,7 @@ int smooth_impl(dg_ctx *c, int l, double *u, const double *f, int steps, bool ze
     int st = fdm_impl(c, l, rin, s);
     if (st) return st;
     LAUNCHK(c, K_FOLD, l, s, pmg::launch_fold(d, Z, u, zero, emit ? T : nullptr, s));
+    c->launches += pmg::fold_launches(d, emit) - 1;
   }
   if (steps == 0 && zero_init) LAUNCH(c, pmg::launch_zero(u, h.N, s));
   return PMG_OK;
@@ -401,11 +402,12 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
                                                        c->lev[l - 1].n, F[l - 1], s));
     } else {
       if ((st = residual_impl(c, l, U[l], F[l], r, s, nu > 0))) return st;    // l.292
-      if (c->lev[l].o_x1)
+      if (c->lev[l].o_x1) {
         LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict_global(d, c->lev[l - 1].n,
                                        wsp<double>(c, c->lev[l].o_interp), r, F[l - 1],
                                        wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s));
-      else
+        c->launches += 2;                                   // three line-GEMM passes
+      } else
         LAUNCHK(c, K_RESTRICT, l, s, pmg::launch_restrict(d, c->lev[l - 1].n,
                                        wsp<double>(c, c->lev[l].o_interp), r, F[l - 1], s));
     }
@@ -421,11 +423,12 @@ int vcycle_impl(dg_ctx *c, double *u, const double *f, bool zero_top, cudaStream
                                                              wsp<double>(c, c->lev[l].o_T), s));
       tr = true;
     } else {
-      if (c->lev[l].o_x1)
+      if (c->lev[l].o_x1) {
         LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong_global(d, nc, Il, U[l - 1], U[l],
                                        wsp<double>(c, c->lev[l].o_x1), wsp<double>(c, c->lev[l].o_x2), s,
                                        wsp<double>(c, c->lev[l].o_r)));    // r_l is dead here (scratch)
-      else
+        c->launches += 3;                                   // three passes + the vector update
+      } else
         LAUNCHK(c, K_PROLONG, l, s, pmg::launch_prolong(d, nc, Il, U[l - 1], U[l], s));   // l.299
     }
     if ((st = smooth_impl(c, l, U[l], F[l], c->nu2[l], false, s, false, tr))) return st;  // l.301

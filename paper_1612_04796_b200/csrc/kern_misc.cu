@@ -794,16 +794,22 @@ __global__ void k_rhs_sin(LevelDev L, double dx, double dy, double dz, double am
 
 }  // namespace
 
+#ifndef PMG_FOLD_SPLIT_MIN_N
+#define PMG_FOLD_SPLIT_MIN_N 17
+#endif
+// kernels launch_fold issues: 2 when the trace pass runs as its own launch (n >= 17, full grids)
+static bool fold_splits_traces(const LevelDev &L) {
+  return L.n >= PMG_FOLD_SPLIT_MIN_N && L.n <= 20 && L.Ne > 4 * num_sms();
+}
+int fold_launches(const LevelDev &L, bool traces) { return traces && fold_splits_traces(L) ? 2 : 1; }
+
 cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
                         cudaStream_t s) {
   // n >= 17 on full grids: the fold WITHOUT its fused trace phase plus the standalone trace kernel
   // is faster than the fused form (c3: 0.152 + 0.047 against 0.221 ms — the trace phase is bound by
   // shared-memory wavefronts and issue slots, and at the tail of every fold CTA it does not hide
   // under the other CTAs' loads, which are issue-bound themselves: 65 % issue utilisation)
-#ifndef PMG_FOLD_SPLIT_MIN_N
-#define PMG_FOLD_SPLIT_MIN_N 17
-#endif
-  if (T && L.n >= PMG_FOLD_SPLIT_MIN_N && L.n <= 20 && L.Ne > 4 * num_sms()) {
+  if (T && fold_splits_traces(L)) {
     cudaError_t e = launch_fold(L, Z, u, zero, nullptr, s);
     return e ? e : launch_traces(L, u, T, s);
   }

@@ -76,6 +76,7 @@ cudaError_t launch_fdm(const LevelDev &L, const double *r, double *Z, double *sc
 // fold; T != nullptr additionally writes the face traces of the updated u (fused trace kernel)
 cudaError_t launch_fold(const LevelDev &L, const double *Z, double *u, bool zero, double *T,
                         cudaStream_t s);
+int fold_launches(const LevelDev &L, bool traces);   // kernels that call issues (1 or 2)
 cudaError_t launch_restrict(const LevelDev &Lf, int nc, const double *I, const double *rf,
                             double *fc, cudaStream_t s);
 cudaError_t launch_prolong(const LevelDev &Lf, int nc, const double *I, const double *uc,
