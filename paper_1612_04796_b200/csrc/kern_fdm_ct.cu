@@ -38,7 +38,9 @@ struct Shape {
   template <int D> __host__ __device__ static constexpr int s() { return D == 0 ? 1 : (D == 1 ? M0 : S2); }
 };
 
-template <int DIR, class SH, bool FWD, bool QF, class Epi>
+// PIPE (x forward pass only): the warp's own tiles were gathered by the warp itself in two cp.async
+// groups (its first two tiles | the rest); it waits for them here instead of at a block barrier
+template <int DIR, class SH, bool FWD, bool QF, class Epi, bool PIPE = false>
 __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi &epi) {
   constexpr int PD = Other<DIR>::P, QD = Other<DIR>::Q;
   constexpr int m = SH::template m<DIR>(), H = m / 2;
@@ -189,6 +191,7 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
   }
 #else
   int tile = warp;
+  if (PIPE) { cp_async_wait<1>(); __syncwarp(); }
   compute(cE0, cO0);
   for (;;) {
     const int t1 = tile + NW;
@@ -197,6 +200,7 @@ __device__ __forceinline__ void eoc_lines(const double *X, const double *S, Epi 
     epilogue(cE0, cO0);
     if (t1 >= NT) break;
     const int t2 = t1 + NW;
+    if (PIPE) { cp_async_wait<0>(); __syncwarp(); }
     if (t2 < NT) compute(cE0, cO0);
     __syncwarp();
     epilogue(cE1, cO1);
@@ -382,8 +386,42 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
     const long long en = (long long)e + PMG_FDM_PREFETCH;
     if (en < L.Ne && L.Ne * n3 > (8ll << 20)) prefetch_l2_doubles(r + en * n3, n3);
   }
+  cp_async_commit();            // group T: the staged tables
   fdm_offsets(L, e, offs);
   __syncthreads();
+#ifdef PMG_GATHER_PIPE         // diagnostic, measured SLOWER (c3 fdm@l4 1.255 vs 1.186, c5 0.929 vs 0.867): the
+  constexpr bool GPIPE = true;  // tile-ordered copies (8 rows at 8 different z per tile) cost more than the overlap buys
+#else
+  constexpr bool GPIPE = false;
+#endif
+  if (GPIPE) {
+    // Pipelined gather: a warp copies exactly the window rows of ITS tiles of the x forward pass
+    // (8 columns = 8 x-rows per tile, z fastest), first two tiles in one cp.async group, the rest
+    // in a second; the pass then starts on the first tiles while the others are still landing —
+    // no block barrier between gather and pass (the rows a warp reads and overwrites are its own)
+    const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
+    constexpr int NCOL0 = M1 * M2, NT0 = (NCOL0 + 7) / 8, NW = SH::NWS;
+    const int lane = threadIdx.x & 31, warp = SH::wid();
+    auto gather_tile = [&](int t) {
+      for (int i = lane; i < 8 * M0; i += 32) {
+        const int cl = i / M0, a = i - cl * M0;
+        const int n = 8 * t + cl;
+        if (n < NCOL0) {
+          const int b = n / M2, c = n - b * M2;
+          cp_async8(X + a + M0 * b + S2 * c, r + xo[a] + yo[b] + zo[c]);
+        }
+      }
+    };
+    int t = warp;
+    if (t < NT0) gather_tile(t);
+    t += NW;
+    if (t < NT0) gather_tile(t);
+    cp_async_commit();
+    for (t += NW; t < NT0; t += NW) gather_tile(t);
+    cp_async_commit();
+    cp_async_wait<2>();         // this thread's share of the tables
+    __syncthreads();            // tables visible to every warp
+  } else
 #ifdef PMG_GATHER_ROWS
   {   // gather: one warp per window row (M0 <= 32), padded plane stride
     const long long *xo = offs, *yo = offs + M0, *zo = offs + M0 + M1;
@@ -438,13 +476,15 @@ __global__ void __launch_bounds__(Shape<M0, M1, M2, WIDE>::THREADS, Shape<M0, M1
 #endif
   }
 #endif
-  cp_async_wait_all();
-  __syncthreads();
+  if (!GPIPE) {
+    cp_async_wait_all();
+    __syncthreads();
+  }
   PMG_PH(1);
   const Blk B = {{M0, M1, M2}, {1, M0, S2}};
   const double *lamc[3] = {lam[0], lam[1], lam[2]};
   EpiStore st{X, B};
-  eoc_lines<0, SH, true, true>(X, Ss[0], st); __syncthreads();
+  eoc_lines<0, SH, true, true, EpiStore, GPIPE>(X, Ss[0], st); __syncthreads();
   PMG_PH(2);
   eoc_lines<1, SH, true, true>(X, Ss[1], st); __syncthreads();
   PMG_PH(3);
